@@ -1,0 +1,133 @@
+/*
+ * ftblas.h -- C ABI of the B200-native fault-tolerant DGEMM (libftblas.so).
+ *
+ * The operation (PAPER.md = the FT-BLAS paper text, /root/reference/PAPER.md):
+ *   C := alpha * op(A) * op(B) + beta * C,   op(X) = X or X^T,
+ * the Level-3 BLAS DGEMM (PAPER.md "Implementation of DGEMM", line 823; the
+ * op() convention as stated for DGEMV, line 799), in binary64, column-major
+ * BLAS storage: element (r, c) of a matrix with leading dimension ld lives at
+ * p[r + c*ld].
+ *
+ * Fault tolerance (ftblas_dgemm only): Huang-Abraham algorithm-based fault
+ * tolerance (section II.A), fused into the GEMM kernel
+ * (section V.B): checksums A^c = [A; e^T A] and B^r = [B, B e] are
+ * encoded per verification tile (FTBLAS_TILE_M x FTBLAS_TILE_N block of C),
+ * the checksum row e^T C and column C e of the product are accumulated in the
+ * same mainloop as the MMA, and the epilogue compares them with the computed
+ * tile, flags any row/column whose difference "exceeds the round-off
+ * threshold" (line 517), locates the erroneous element at the intersection of
+ * the flagged row and column (line 540) and corrects it before C is stored.
+ * The detection threshold, the multi-flag rule and the correction rule are the
+ * readings R4-R7 of DESIGN.md section 3.
+ *
+ * Conventions for every entry point:
+ *   - A, B, C are DEVICE pointers (cudaMalloc'ed or torch CUDA storage) on the
+ *     current CUDA device, except in ftblas_dgemm_host where they are HOST
+ *     pointers.  The caller owns all memory; the library owns only its
+ *     internal workspace and report buffers (freed by ftblas_release).
+ *   - transA/transB: 'N'/'n' (op(X) = X) or 'T'/'t'/'C'/'c' (op(X) = X^T).
+ *   - op(A) is M x K: A is M x K (lda >= max(1,M)) for 'N', K x M (lda >= max(1,K)) for 'T'.
+ *     op(B) is K x N: B is K x N (ldb >= max(1,K)) for 'N', N x K (ldb >= max(1,N)) for 'T'.
+ *     C is M x N, ldc >= max(1,M).
+ *   - beta == 0: C is not read on input (may hold NaN); alpha == 0: A and B are
+ *     not read.  M == 0 or N == 0: no-op.
+ *   - Work is enqueued on the stream set by ftblas_set_stream (default: the
+ *     legacy default stream).  Calls are asynchronous unless they take a
+ *     non-NULL report (see below).
+ *   - Return value: 0 on success; -p if argument p (1-based, BLAS xerbla
+ *     numbering) is invalid; FTBLAS_ERR_CUDA (1000) on a CUDA error, with the
+ *     message available from ftblas_last_error().  Nothing is launched when an
+ *     argument is invalid.
+ *   - Not thread-safe: one host thread drives the library per process (one
+ *     process per GPU).
+ */
+#ifndef FTBLAS_H
+#define FTBLAS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FTBLAS_TILE_M 128 /* verification tile rows (one CTA tile of C) */
+#define FTBLAS_TILE_N 128 /* verification tile columns */
+#define FTBLAS_ERR_CUDA 1000
+
+/* One corrected element of C.  Field order/size is ABI (48 bytes). */
+typedef struct ftblas_correction {
+    int64_t tile_m;   /* verification tile row index    (= i / FTBLAS_TILE_M) */
+    int64_t tile_n;   /* verification tile column index (= j / FTBLAS_TILE_N) */
+    int64_t i, j;     /* 0-based row / column of the corrected element of C */
+    double residual;  /* row-checksum residual d_i of row i (sum_j C_ij - (C e)_i) */
+    int32_t kind;     /* 1: exactly one row and one column flagged in the tile -> their
+                         intersection (Huang-Abraham location);
+                         2: several flags -> candidate recomputation (reading R7) */
+    int32_t pad;
+} ftblas_correction;
+
+/* Error report of one ftblas_dgemm call.  entries/capacity are supplied by the
+ * caller (HOST memory, may be NULL/0); the library fills the rest.  Entries are
+ * unordered (tiles run concurrently); sort by (tile_n, tile_m, j, i) to compare. */
+typedef struct ftblas_err_report {
+    ftblas_correction *entries; /* in: host array of `capacity` records (caller-owned) */
+    int64_t capacity;           /* in */
+    int64_t count;              /* out: corrections made (may exceed capacity: truncated) */
+    int64_t tiles_flagged;      /* out: tiles with >= 1 flagged row or column */
+    int64_t rows_flagged;       /* out: flagged rows summed over tiles */
+    int64_t cols_flagged;       /* out: flagged columns summed over tiles */
+} ftblas_err_report;
+
+/* ABFT DGEMM (the hot path).  Device pointers.  If err_report != NULL the call
+ * synchronizes the stream and fills *err_report; if NULL it is fully
+ * asynchronous and the report can be read later with ftblas_report_fetch.
+ * Corrections are applied to C in both cases.  Faults from the plan installed
+ * by ftblas_set_fault_plan are injected into the accumulator before
+ * verification (test/benchmark harness; empty plan = no injection). */
+int ftblas_dgemm(char transA, char transB, int64_t M, int64_t N, int64_t K, double alpha,
+                 const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
+                 double *C, int64_t ldc, ftblas_err_report *err_report);
+
+/* The same DGEMM without fault tolerance (same tiles and mainloop, no checksums,
+ * no verification, no injection): the baseline for the FT overhead. */
+int ftblas_dgemm_noft(char transA, char transB, int64_t M, int64_t N, int64_t K, double alpha,
+                      const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
+                      double *C, int64_t ldc);
+
+/* ftblas_dgemm on HOST buffers (end-to-end path): copies op(A), op(B) and C
+ * (if beta != 0) host->device, runs ftblas_dgemm, copies C device->host and
+ * synchronizes.  err_report as above (may be NULL).  Pinned host memory gives
+ * the full PCIe bandwidth; pageable memory works but is slower. */
+int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K, double alpha,
+                      const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
+                      double *C, int64_t ldc, ftblas_err_report *err_report);
+
+/* Read the report of the most recent ftblas_dgemm call (synchronizes the stream). */
+int ftblas_report_fetch(ftblas_err_report *err_report);
+
+/* Install a fault-injection plan for subsequent ftblas_dgemm calls: n single-bit
+ * flips, flip k toggles bit bit[k] (0..63) of the accumulator of element
+ * (i[k], j[k]) of C (0-based, 0 <= i < M, 0 <= j < N of the call) before the
+ * epilogue.  Host arrays, copied.  n == 0 clears the plan.  Plans are matched
+ * against the M x N of each call; entries outside it are ignored. */
+int ftblas_set_fault_plan(int64_t n, const int64_t *i, const int64_t *j, const int32_t *bit);
+
+/* Stream for subsequent calls (a cudaStream_t passed as void*; NULL = default stream). */
+int ftblas_set_stream(void *stream);
+
+/* Number of kernels the library launched since load (for launch accounting). */
+int64_t ftblas_launch_count(void);
+
+/* Verification tile shape (FTBLAS_TILE_M, FTBLAS_TILE_N). */
+void ftblas_tile_shape(int32_t *tile_m, int32_t *tile_n);
+
+/* Message of the last error (static storage, never NULL). */
+const char *ftblas_last_error(void);
+
+/* Free the library's device workspace (it is re-allocated on demand). */
+int ftblas_release(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FTBLAS_H */

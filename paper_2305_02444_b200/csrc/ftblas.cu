@@ -1,0 +1,339 @@
+// ftblas.cu -- host side of libftblas.so: the C ABI declared in include/ftblas.h.
+//
+// Argument checking (BLAS xerbla numbering), workspace management, fault-plan
+// upload (CSR by verification tile), kernel selection by transpose/alignment,
+// launches on the caller's stream, report readback.  All arithmetic of the hot
+// path runs in the kernels of ftblas_kernels.cuh.
+#include "ftblas_kernels.cuh"
+#include "../../include/ftblas.h"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+namespace {
+
+using namespace ftb;
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t need) {
+        if (need <= bytes) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&p, need);
+        if (e == cudaSuccess) bytes = need;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
+struct Ctx {
+    cudaStream_t stream = nullptr;
+    DevBuf ws;            // encode outputs
+    DevBuf rep;           // ReportHdr + entries
+    long long rep_cap = 1 << 16;
+    DevBuf plan_dev;      // fault plan arrays
+    DevBuf plan_ptr_dev;  // CSR offsets for the last (M,N) shape
+    long long plan_ptr_M = -1, plan_ptr_N = -1, plan_version = 0, plan_uploaded = -1;
+    long long plan_n_dev = 0;
+    std::vector<long long> plan_i, plan_j;
+    std::vector<int> plan_bit;
+    DevBuf hA, hB, hC;    // ftblas_dgemm_host device staging
+    long long launches = 0;
+    char err[512] = "no error";
+    int device = -1;
+};
+Ctx &ctx() {
+    static Ctx c;
+    return c;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+    snprintf(ctx().err, sizeof(ctx().err), "%s: %s", what, cudaGetErrorString(e));
+    return FTBLAS_ERR_CUDA;
+}
+int arg_fail(int p, const char *what) {
+    snprintf(ctx().err, sizeof(ctx().err), "invalid argument %d: %s", p, what);
+    return -p;
+}
+
+#define CK(call, what)                                   \
+    do {                                                 \
+        cudaError_t _e = (call);                         \
+        if (_e != cudaSuccess) return cuda_fail(_e, what); \
+    } while (0)
+
+bool trans_ok(char t) { return t == 'N' || t == 'n' || t == 'T' || t == 't' || t == 'C' || t == 'c'; }
+bool is_t(char t) { return !(t == 'N' || t == 'n'); }
+
+int check_args(char ta, char tb, long long M, long long N, long long K, const void *A, long long lda,
+               const void *B, long long ldb, const void *C, long long ldc, double alpha, double beta) {
+    if (!trans_ok(ta)) return arg_fail(1, "transA");
+    if (!trans_ok(tb)) return arg_fail(2, "transB");
+    if (M < 0) return arg_fail(3, "M < 0");
+    if (N < 0) return arg_fail(4, "N < 0");
+    if (K < 0) return arg_fail(5, "K < 0");
+    const long long nrowa = is_t(ta) ? K : M, nrowb = is_t(tb) ? N : K;
+    if (lda < std::max<long long>(1, nrowa)) return arg_fail(8, "lda too small");
+    if (ldb < std::max<long long>(1, nrowb)) return arg_fail(10, "ldb too small");
+    if (ldc < std::max<long long>(1, M)) return arg_fail(13, "ldc too small");
+    if (M > 0 && N > 0 && K > 0 && alpha != 0.0) {
+        if (!A) return arg_fail(7, "A is NULL");
+        if (!B) return arg_fail(9, "B is NULL");
+    }
+    if (M > 0 && N > 0 && !C) return arg_fail(12, "C is NULL");
+    (void)beta;
+    return 0;
+}
+
+template <bool KCA, bool KCB, bool VA, bool VB, bool FT>
+cudaError_t launch_gemm_t(const GemmArgs &g, long long tiles, cudaStream_t s) {
+    auto kern = gemm_kernel<KCA, KCB, VA, VB, FT>;
+    const int bytes = SmemPlan<KCA, KCB, FT>::BYTES;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)tiles, NTHREADS, bytes, s>>>(g);
+    ctx().launches++;
+    return cudaGetLastError();
+}
+
+template <bool FT>
+cudaError_t launch_gemm(bool kca, bool kcb, bool va, bool vb, const GemmArgs &g, long long tiles, cudaStream_t s) {
+    // 16 instantiations: transpose layout x 16-byte vector loads
+#define L(a, b, c, d) if (kca == a && kcb == b && va == c && vb == d) return launch_gemm_t<a, b, c, d, FT>(g, tiles, s)
+    L(false, true, true, true); L(false, false, true, true); L(true, true, true, true); L(true, false, true, true);
+    L(false, true, false, true); L(false, false, false, true); L(true, true, false, true); L(true, false, false, true);
+    L(false, true, true, false); L(false, false, true, false); L(true, true, true, false); L(true, false, true, false);
+    L(false, true, false, false); L(false, false, false, false); L(true, true, false, false); L(true, false, false, false);
+#undef L
+    return cudaErrorInvalidValue;
+}
+
+bool vec_ok(const void *p, long long ld) {
+    return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && (ld % 2 == 0);
+}
+
+// Upload the CSR (by tile, tile index tn*ntm + tm) of the fault plan restricted to M x N.
+int prepare_plan(long long M, long long N, GemmArgs &g) {
+    Ctx &c = ctx();
+    g.plan_ptr = nullptr; g.plan_i = nullptr; g.plan_j = nullptr; g.plan_bit = nullptr;
+    if (c.plan_i.empty()) return 0;
+    const size_t bytes_ij0 = std::max<size_t>(1, c.plan_i.size()) * sizeof(long long);
+    if (c.plan_uploaded == c.plan_version && c.plan_ptr_M == M && c.plan_ptr_N == N) {  // cached upload
+        char *base = c.plan_dev.as<char>();
+        g.plan_ptr = c.plan_ptr_dev.as<int>();
+        g.plan_i = reinterpret_cast<const long long *>(base);
+        g.plan_j = reinterpret_cast<const long long *>(base + bytes_ij0);
+        g.plan_bit = reinterpret_cast<const int *>(base + 2 * bytes_ij0);
+        return 0;
+    }
+    const long long ntm = (M + BM - 1) / BM, ntn = (N + BN - 1) / BN, nt = ntm * ntn;
+    std::vector<int> cnt(nt + 1, 0);
+    std::vector<long long> order;
+    for (size_t f = 0; f < c.plan_i.size(); f++) {
+        const long long i = c.plan_i[f], j = c.plan_j[f];
+        if (i < 0 || i >= M || j < 0 || j >= N) continue;
+        cnt[(j / BN) * ntm + i / BM + 1]++;
+        order.push_back((long long)f);
+    }
+    for (long long t = 0; t < nt; t++) cnt[t + 1] += cnt[t];
+    std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+    const size_t n = order.size();
+    std::vector<long long> pi(n), pj(n);
+    std::vector<int> pb(n);
+    for (long long f : order) {
+        const long long i = c.plan_i[f], j = c.plan_j[f];
+        const int pos = fill[(j / BN) * ntm + i / BM]++;
+        pi[pos] = i; pj[pos] = j; pb[pos] = c.plan_bit[f];
+    }
+    const size_t bytes_ij = bytes_ij0;  // sized by the full plan so the cached layout is stable
+    const size_t bytes_b = std::max<size_t>(1, c.plan_i.size()) * sizeof(int);
+    CK(c.plan_dev.ensure(2 * bytes_ij + bytes_b), "cudaMalloc(plan)");
+    CK(c.plan_ptr_dev.ensure((nt + 1) * sizeof(int)), "cudaMalloc(plan_ptr)");
+    char *base = c.plan_dev.as<char>();
+    // synchronous copies: the plan is host-side test-harness state, uploaded before the launch
+    CK(cudaMemcpyAsync(base, pi.data(), n * sizeof(long long), cudaMemcpyHostToDevice, c.stream), "plan i");
+    CK(cudaMemcpyAsync(base + bytes_ij, pj.data(), n * sizeof(long long), cudaMemcpyHostToDevice, c.stream), "plan j");
+    CK(cudaMemcpyAsync(base + 2 * bytes_ij, pb.data(), n * sizeof(int), cudaMemcpyHostToDevice, c.stream), "plan bit");
+    CK(cudaMemcpyAsync(c.plan_ptr_dev.p, cnt.data(), (nt + 1) * sizeof(int), cudaMemcpyHostToDevice, c.stream), "plan ptr");
+    CK(cudaStreamSynchronize(c.stream), "plan upload");
+    c.plan_uploaded = c.plan_version; c.plan_ptr_M = M; c.plan_ptr_N = N;
+    g.plan_ptr = c.plan_ptr_dev.as<int>();
+    g.plan_i = reinterpret_cast<const long long *>(base);
+    g.plan_j = reinterpret_cast<const long long *>(base + bytes_ij);
+    g.plan_bit = reinterpret_cast<const int *>(base + 2 * bytes_ij);
+    return 0;
+}
+
+int fetch_report(ftblas_err_report *r) {
+    Ctx &c = ctx();
+    CK(cudaStreamSynchronize(c.stream), "report sync");
+    ReportHdr h{};
+    if (c.rep.p) CK(cudaMemcpy(&h, c.rep.p, sizeof(h), cudaMemcpyDeviceToHost), "report header");
+    r->count = (int64_t)h.count;
+    r->tiles_flagged = (int64_t)h.tiles_flagged;
+    r->rows_flagged = (int64_t)h.rows_flagged;
+    r->cols_flagged = (int64_t)h.cols_flagged;
+    const long long n = std::min<long long>({(long long)h.count, (long long)r->capacity, c.rep_cap});
+    if (n > 0 && r->entries)
+        CK(cudaMemcpy(r->entries, c.rep.as<char>() + sizeof(ReportHdr), n * sizeof(Correction),
+                      cudaMemcpyDeviceToHost), "report entries");
+    return 0;
+}
+
+int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K, double alpha,
+               const double *A, long long lda, const double *B, long long ldb, double beta, double *C,
+               long long ldc, ftblas_err_report *rep) {
+    static_assert(sizeof(Correction) == sizeof(ftblas_correction), "ABI");
+    Ctx &c = ctx();
+    int rc = check_args(ta, tb, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta);
+    if (rc) return rc;
+    if (ft) {
+        CK(c.rep.ensure(sizeof(ReportHdr) + c.rep_cap * sizeof(Correction)), "cudaMalloc(report)");
+    }
+    if (M == 0 || N == 0) {
+        if (ft) CK(cudaMemsetAsync(c.rep.p, 0, sizeof(ReportHdr), c.stream), "report reset");
+        return rep ? fetch_report(rep) : 0;
+    }
+    const bool kca = is_t(ta), kcb = !is_t(tb);
+    const long long ntm = (M + BM - 1) / BM, ntn = (N + BN - 1) / BN;
+    GemmArgs g{};
+    g.A = A; g.B = B; g.C = C; g.lda = lda; g.ldb = ldb; g.ldc = ldc;
+    g.M = M; g.N = N; g.K = K; g.alpha = alpha; g.beta = beta;
+    const bool va = vec_ok(A, lda), vb = vec_ok(B, ldb);
+    if (ft) {
+        const long long Kp = std::max<long long>(16, (K + 15) / 16 * 16);
+        // k-chunks of the encode pass: enough blocks to fill the GPU, chunks >= 32 columns
+        int kch = (int)std::max<long long>(1, std::min<long long>(16, (2 * 148 + ntm + ntn - 1) / (ntm + ntn)));
+        kch = (int)std::min<long long>(kch, std::max<long long>(1, Kp / 32));
+        const long long kper = ((Kp + kch - 1) / kch + 31) / 32 * 32;
+        const size_t nV = (size_t)(ntm + ntn) * Kp, nLine = (size_t)kch * (M + N), nT = (size_t)kch * (ntm + ntn);
+        CK(c.ws.ensure((nV + nLine + nT) * sizeof(double)), "cudaMalloc(workspace)");
+        double *w = c.ws.as<double>();
+        g.VA = w; g.WB = w + ntm * Kp;
+        double *lineA = w + nV, *lineB = lineA + (size_t)kch * M;
+        double *tmaxA = lineB + (size_t)kch * N, *tmaxB = tmaxA + (size_t)kch * ntm;
+        g.lineA = lineA; g.lineB = lineB; g.tmaxA = tmaxA; g.tmaxB = tmaxB;
+        g.kch = kch; g.Kp = Kp;
+        g.rep = c.rep.as<ReportHdr>();
+        g.rep_entries = reinterpret_cast<Correction *>(c.rep.as<char>() + sizeof(ReportHdr));
+        g.rep_cap = c.rep_cap;
+        rc = prepare_plan(M, N, g);
+        if (rc) return rc;
+        EncodeArgs ea{};
+        ea.op[0] = EncodeOperand{A, lda, M, kca ? 1 : 0, const_cast<double *>(g.VA), lineA, tmaxA, (int)ntm};
+        ea.op[1] = EncodeOperand{B, ldb, N, kcb ? 1 : 0, const_cast<double *>(g.WB), lineB, tmaxB, (int)ntn};
+        ea.K = (alpha == 0.0) ? 0 : K;  // alpha == 0: A, B are not read (encodes are zero)
+        ea.Kp = Kp; ea.kper = kper; ea.kch = kch; ea.rep = g.rep;
+        dim3 grid((unsigned)std::max(ntm, ntn), (unsigned)kch, 2);
+        encode_kernel<<<grid, NTHREADS, 0, c.stream>>>(ea);
+        c.launches++;
+        CK(cudaGetLastError(), "encode_kernel launch");
+        CK(launch_gemm<true>(kca, kcb, va, vb, g, ntm * ntn, c.stream), "gemm_kernel<FT> launch");
+    } else {
+        CK(launch_gemm<false>(kca, kcb, va, vb, g, ntm * ntn, c.stream), "gemm_kernel launch");
+    }
+    if (rep) return fetch_report(rep);
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ftblas_dgemm(char transA, char transB, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
+                 int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,
+                 ftblas_err_report *err_report) {
+    return dgemm_impl(true, transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, err_report);
+}
+
+int ftblas_dgemm_noft(char transA, char transB, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
+                      int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc) {
+    return dgemm_impl(false, transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, nullptr);
+}
+
+int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
+                      int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,
+                      ftblas_err_report *err_report) {
+    Ctx &c = ctx();
+    int rc = check_args(transA, transB, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta);
+    if (rc) return rc;
+    if (M == 0 || N == 0) return dgemm_impl(true, transA, transB, M, N, K, alpha, nullptr, lda, nullptr, ldb,
+                                            beta, nullptr, ldc, err_report);
+    const long long ar = is_t(transA) ? K : M, ac = is_t(transA) ? M : K;
+    const long long br = is_t(transB) ? N : K, bc = is_t(transB) ? K : N;
+    const bool readAB = K > 0 && alpha != 0.0;
+    // device copies are packed (ld = rows, rounded to even for 16-byte vector loads)
+    const long long dla = std::max<long long>(1, (ar + 1) / 2 * 2), dlb = std::max<long long>(1, (br + 1) / 2 * 2);
+    const long long dlc = std::max<long long>(1, (M + 1) / 2 * 2);
+    if (readAB) {
+        CK(c.hA.ensure((size_t)dla * ac * 8), "cudaMalloc(A)");
+        CK(c.hB.ensure((size_t)dlb * bc * 8), "cudaMalloc(B)");
+        CK(cudaMemcpy2DAsync(c.hA.p, dla * 8, A, lda * 8, ar * 8, ac, cudaMemcpyHostToDevice, c.stream), "H2D A");
+        CK(cudaMemcpy2DAsync(c.hB.p, dlb * 8, B, ldb * 8, br * 8, bc, cudaMemcpyHostToDevice, c.stream), "H2D B");
+    }
+    CK(c.hC.ensure((size_t)dlc * N * 8), "cudaMalloc(C)");
+    if (beta != 0.0)
+        CK(cudaMemcpy2DAsync(c.hC.p, dlc * 8, C, ldc * 8, M * 8, N, cudaMemcpyHostToDevice, c.stream), "H2D C");
+    rc = dgemm_impl(true, transA, transB, M, N, K, alpha, readAB ? c.hA.as<double>() : nullptr, readAB ? dla : std::max<long long>(1, ar),
+                    readAB ? c.hB.as<double>() : nullptr, readAB ? dlb : std::max<long long>(1, br), beta, c.hC.as<double>(), dlc,
+                    nullptr);
+    if (rc) return rc;
+    CK(cudaMemcpy2DAsync(C, ldc * 8, c.hC.p, dlc * 8, M * 8, N, cudaMemcpyDeviceToHost, c.stream), "D2H C");
+    if (err_report) return fetch_report(err_report);
+    CK(cudaStreamSynchronize(c.stream), "sync");
+    return 0;
+}
+
+int ftblas_report_fetch(ftblas_err_report *err_report) {
+    if (!err_report) return arg_fail(1, "err_report is NULL");
+    return fetch_report(err_report);
+}
+
+int ftblas_set_fault_plan(int64_t n, const int64_t *i, const int64_t *j, const int32_t *bit) {
+    Ctx &c = ctx();
+    if (n < 0) return arg_fail(1, "n < 0");
+    if (n > 0 && (!i || !j || !bit)) return arg_fail(2, "NULL plan array");
+    for (int64_t f = 0; f < n; f++)
+        if (bit[f] < 0 || bit[f] > 63) return arg_fail(4, "bit out of [0,63]");
+    c.plan_i.assign(i, i + n);
+    c.plan_j.assign(j, j + n);
+    c.plan_bit.assign(bit, bit + n);
+    c.plan_version++;
+    return 0;
+}
+
+int ftblas_set_stream(void *stream) {
+    ctx().stream = static_cast<cudaStream_t>(stream);
+    return 0;
+}
+
+int64_t ftblas_launch_count(void) { return ctx().launches; }
+
+void ftblas_tile_shape(int32_t *tile_m, int32_t *tile_n) {
+    if (tile_m) *tile_m = FTBLAS_TILE_M;
+    if (tile_n) *tile_n = FTBLAS_TILE_N;
+}
+
+const char *ftblas_last_error(void) { return ctx().err; }
+
+int ftblas_release(void) {
+    Ctx &c = ctx();
+    cudaStreamSynchronize(c.stream);
+    c.ws.release(); c.rep.release(); c.plan_dev.release(); c.plan_ptr_dev.release();
+    c.plan_uploaded = -1;
+    c.hA.release(); c.hB.release(); c.hC.release();
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,276 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star):
+  * error reports bit-exact: the same (tile, i, j) list (+ kind) and the same count;
+  * corrected C within 4 (K+2) 2^-53 (|alpha| |A||B| + |beta| |C0|) elementwise.
+Small cases compare every element; full-size configs compare the tiles the oracle can
+compute (every faulty tile of configs[1], samples elsewhere) plus sampled elements.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synthetic as syn
+from tests._util import from_dev, gemm_bound, report_key, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ft():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2305_02444_b200 import ftblas
+    ftblas.ftblas_set_stream(None)
+    return ftblas
+
+
+def run_gpu(ft, w, d, *, plan=None, noft=False, offsets=(0, 0, 0)):
+    A_t, pA = to_dev(d["A"], offsets[0])
+    B_t, pB = to_dev(d["B"], offsets[1])
+    C_t, pC = to_dev(d["C"], offsets[2])
+    if plan is not None:
+        ft.ftblas_set_fault_plan(*plan)
+    else:
+        ft.ftblas_clear_fault_plan()
+    rep = ft.Report(8192)
+    if noft:
+        ft.ftblas_dgemm_noft(w.transA, w.transB, w.M, w.N, w.K, w.alpha, pA, d["lda"], pB, d["ldb"],
+                             w.beta, pC, d["ldc"])
+        import torch
+        torch.cuda.synchronize()
+        rep = None
+    else:
+        ft.ftblas_dgemm(w.transA, w.transB, w.M, w.N, w.K, w.alpha, pA, d["lda"], pB, d["ldb"],
+                        w.beta, pC, d["ldc"], rep)
+    ft.ftblas_clear_fault_plan()
+    return from_dev(C_t, d["C"], offsets[2]), rep
+
+
+def run_oracle(w, d, plan=None, tiles_only=None):
+    C = np.array(syn.base_of(d["C"]), order="F", copy=True)[: w.M, :]
+    Cb = np.asfortranarray(syn.base_of(d["C"]).copy())
+    Cv = Cb[: w.M, :]
+    rep, st = oracle.abft_dgemm(w.transA, w.transB, w.M, w.N, w.K, w.alpha, d["A"], d["lda"],
+                                d["B"], d["ldb"], w.beta, Cv, d["ldc"], faults=plan,
+                                cap=max(64, 4 * (0 if plan is None else len(plan[0]))),
+                                tiles_only=tiles_only)
+    return Cv, rep, st
+
+
+def abs_product(w, d):
+    opA = d["A"] if w.transA == "N" else d["A"].T
+    opB = d["B"] if w.transB == "N" else d["B"].T
+    return np.abs(opA) @ np.abs(opB)
+
+
+def assert_close(w, d, C_gpu, C_ref, rows=None, cols=None):
+    ab = abs_product(w, d)
+    c0 = np.abs(d["C"]) if w.beta != 0 else np.zeros_like(ab)
+    tol = gemm_bound(w.K, w.alpha, w.beta, ab, c0)
+    err = np.abs(C_gpu - C_ref)
+    bad = ~(err <= tol)
+    assert not bad.any(), f"{bad.sum()} elements beyond tolerance; max err {err.max()}"
+
+
+SMALL = [
+    # (M, N, K, tA, tB, alpha, beta, dist, pad)
+    (300, 260, 70, "N", "N", 1.0, 0.0, "uniform", 0),
+    (300, 260, 70, "N", "T", 1.5, -0.5, "uniform", 0),
+    (257, 129, 33, "T", "N", -1.0, 1.0, "normal", 0),
+    (130, 390, 100, "T", "T", 0.75, 2.0, "uniform", 3),
+    (128, 128, 16, "N", "N", 1.0, 0.0, "uniform", 0),
+    (1, 1, 1, "N", "N", 2.0, 0.0, "uniform", 0),
+    (5, 700, 9, "N", "T", 1.0, 1.0, "normal", 1),
+    (700, 3, 17, "T", "N", 1.0, 0.0, "uniform", 0),
+]
+
+
+@pytest.mark.parametrize("case", SMALL)
+def test_fault_free_matches_oracle(ft, case):
+    M, N, K, tA, tB, al, be, dist, pad = case
+    w = syn.Workload("t", M, N, K, tA, tB, al, be, dist, True, seed=M * 7 + N + K)
+    d = syn.make_inputs(w, pad=pad)
+    C_gpu, rep = run_gpu(ft, w, d)
+    C_ref, orep, st = run_oracle(w, d)
+    assert rep.count == 0 and rep.tiles_flagged == 0 and orep == []
+    assert_close(w, d, C_gpu, C_ref)
+    C_nf, _ = run_gpu(ft, w, d, noft=True)
+    assert_close(w, d, C_nf, C_ref)
+
+
+@pytest.mark.parametrize("offsets", [(1, 0, 0), (0, 1, 1), (1, 1, 1)])
+def test_misaligned_and_odd_ld(ft, offsets):
+    """8-byte (non-vector) staging path: misaligned pointers and odd leading dimensions."""
+    w = syn.Workload("t", 201, 150, 45, "N", "T", 1.25, -1.0, "uniform", True, seed=5)
+    d = syn.make_inputs(w, pad=1)  # ld = rows + 1 (odd for even rows)
+    plan = syn.fault_plan(w.M, w.N, 2, 9)
+    C_gpu, rep = run_gpu(ft, w, d, plan=plan, offsets=offsets)
+    C_ref, orep, _ = run_oracle(w, d, plan)
+    assert report_key(rep.entries()) == report_key(orep)
+    assert_close(w, d, C_gpu, C_ref)
+
+
+@pytest.mark.parametrize("tA,tB", [("N", "N"), ("N", "T"), ("T", "N"), ("T", "T")])
+def test_injected_flips_reports_bit_exact(ft, tA, tB):
+    w = syn.Workload("t", 390, 300, 130, tA, tB, 1.5, -0.5, "uniform", True, seed=11)
+    d = syn.make_inputs(w)
+    plan = syn.fault_plan(w.M, w.N, 9, 21)
+    C_gpu, rep = run_gpu(ft, w, d, plan=plan)
+    C_ref, orep, st = run_oracle(w, d, plan)
+    assert rep.count == st.count == 9
+    assert report_key(rep.entries()) == report_key(orep)
+    assert (rep.tiles_flagged, rep.rows_flagged, rep.cols_flagged) == \
+        (st.tiles_flagged, st.rows_flagged, st.cols_flagged)
+    assert_close(w, d, C_gpu, C_ref)
+
+
+def test_multiple_errors_in_one_tile(ft):
+    """Two flips in one tile (distinct rows/cols) and two in one row: candidate path (kind 2)."""
+    w = syn.Workload("t", 256, 256, 64, "N", "N", 1.0, 0.0, "uniform", False, seed=3)
+    d = syn.make_inputs(w)
+    plan = (np.array([3, 40, 200, 200], np.int64), np.array([10, 55, 130, 250], np.int64),
+            np.array([50, 58, 45, 61], np.int32))
+    C_gpu, rep = run_gpu(ft, w, d, plan=plan)
+    C_ref, orep, st = run_oracle(w, d, plan)
+    assert report_key(rep.entries()) == report_key(orep)
+    assert sorted((e["i"], e["j"]) for e in rep.entries()) == [(3, 10), (40, 55), (200, 130), (200, 250)]
+    assert_close(w, d, C_gpu, C_ref)
+
+
+@pytest.mark.parametrize("bit", [40, 47, 51, 52, 55, 60, 61, 62])
+def test_each_bit_class(ft, bit):
+    w = syn.Workload("t", 256, 256, 200, "N", "N", 1.0, 0.0, "normal", False, seed=bit)
+    d = syn.make_inputs(w)
+    rng = np.random.default_rng(bit)
+    plan = (np.array([rng.integers(256)], np.int64), np.array([rng.integers(256)], np.int64),
+            np.array([bit], np.int32))
+    C_gpu, rep = run_gpu(ft, w, d, plan=plan)
+    C_ref, orep, _ = run_oracle(w, d, plan)
+    assert report_key(rep.entries()) == report_key(orep)
+    assert rep.count == 1
+    assert_close(w, d, C_gpu, C_ref)
+
+
+def test_degenerate_shapes(ft):
+    import torch
+    # M == 0 / N == 0: no-op, empty report
+    z = torch.zeros(4, dtype=torch.float64, device="cuda")
+    rep = ft.Report(4)
+    ft.ftblas_dgemm("N", "N", 0, 5, 3, 1.0, z, 1, z, 3, 0.0, z, 1, rep)
+    assert rep.count == 0
+    # K == 0: C := beta C;  alpha == 0: A, B not read (NULL)
+    w = syn.Workload("t", 140, 70, 0, "N", "N", 1.0, 2.0, "uniform", True, seed=1)
+    d = syn.make_inputs(w)
+    C_t, pC = to_dev(d["C"])
+    ft.ftblas_dgemm("N", "N", 140, 70, 0, 1.0, None, 140, None, 1, 2.0, pC, 140, rep)
+    assert rep.count == 0
+    assert np.array_equal(from_dev(C_t, d["C"]), 2.0 * d["C"])
+    C_t, pC = to_dev(d["C"])
+    ft.ftblas_dgemm("N", "N", 140, 70, 9, 0.0, None, 140, None, 9, -1.0, pC, 140, rep)
+    assert np.array_equal(from_dev(C_t, d["C"]), -d["C"])
+
+
+def test_beta_zero_ignores_nan_in_C(ft):
+    w = syn.Workload("t", 150, 140, 20, "N", "N", 1.0, 0.0, "uniform", False, seed=2)
+    d = syn.make_inputs(w)
+    d["C"] = np.asfortranarray(np.full((150, 140), np.nan))
+    C_gpu, rep = run_gpu(ft, w, d)
+    assert np.isfinite(C_gpu).all() and rep.count == 0
+
+
+def test_host_buffer_entry_point(ft):
+    w = syn.CONFIGS[0]
+    d = syn.make_inputs(w)
+    plan = syn.fault_plan(w.M, w.N, w.n_flips, w.seed)
+    ft.ftblas_set_fault_plan(*plan)
+    C = np.asfortranarray(d["C"].copy())
+    rep = ft.Report(64)
+    ft.ftblas_dgemm_host(w.transA, w.transB, w.M, w.N, w.K, w.alpha, np.asfortranarray(d["A"]),
+                         d["lda"], np.asfortranarray(d["B"]), d["ldb"], w.beta, C, d["ldc"], rep)
+    ft.ftblas_clear_fault_plan()
+    C_ref, orep, _ = run_oracle(w, d, plan)
+    assert report_key(rep.entries()) == report_key(orep)
+    assert_close(w, d, C, C_ref)
+
+
+# ---------------------------------------------------------------- BASELINE configs
+def test_config0_all_flips_corrected(ft):
+    w = syn.CONFIGS[0]
+    d = syn.make_inputs(w)
+    plan = syn.fault_plan(w.M, w.N, w.n_flips, w.seed)
+    C_gpu, rep = run_gpu(ft, w, d, plan=plan)
+    C_ref, orep, st = run_oracle(w, d, plan)
+    assert rep.count == st.count == w.n_flips
+    assert report_key(rep.entries()) == report_key(orep)
+    assert sorted((e["i"], e["j"]) for e in rep.entries()) == sorted(zip(*[p.tolist() for p in plan[:2]]))
+    assert_close(w, d, C_gpu, C_ref)
+
+
+def sampled_check(w, d, C_gpu, n=300, seed=0, extra=()):
+    rng = np.random.default_rng(seed)
+    pts = [(int(rng.integers(w.M)), int(rng.integers(w.N))) for _ in range(n)] + list(extra)
+    for (i, j) in pts:
+        acc = oracle.dot(w.transA, w.transB, w.K, d["A"], d["lda"], d["B"], d["ldb"], i, j)
+        ab = oracle.absdot(w.transA, w.transB, w.K, d["A"], d["lda"], d["B"], d["ldb"], i, j)
+        c0 = d["C"][i, j] if w.beta != 0 else 0.0
+        ref = w.alpha * acc + (w.beta * c0 if w.beta != 0 else 0.0)
+        tol = gemm_bound(w.K, w.alpha, w.beta, ab, abs(c0))
+        assert abs(C_gpu[i, j] - ref) <= tol, (i, j, C_gpu[i, j], ref)
+
+
+def tile_mask(w, plan, limit=None):
+    ntm, ntn = -(-w.M // 128), -(-w.N // 128)
+    mask = np.zeros(ntm * ntn, np.uint8)
+    sel = list(zip(plan[0].tolist(), plan[1].tolist()))[:limit]
+    for i, j in sel:
+        mask[(j // 128) * ntm + i // 128] = 1
+    return mask, sel
+
+
+def check_full_config(ft, w, oracle_tiles=None):
+    d = syn.make_inputs(w)
+    plan = syn.fault_plan(w.M, w.N, w.n_flips, w.seed)
+    # fault-free run: no report, sampled elements within tolerance
+    C_clean, rep0 = run_gpu(ft, w, d)
+    assert rep0.count == 0 and rep0.tiles_flagged == 0
+    sampled_check(w, d, C_clean, n=100)
+    # injected run
+    C_gpu, rep = run_gpu(ft, w, d, plan=plan)
+    got = report_key(rep.entries())
+    assert rep.count == w.n_flips
+    assert sorted((g[2], g[3]) for g in got) == sorted(zip(plan[0].tolist(), plan[1].tolist()))
+    # oracle on the faulty tiles it can afford
+    mask, sel = tile_mask(w, plan, oracle_tiles)
+    C_or, orep, st = run_oracle(w, d, plan, tiles_only=mask)
+    sel_tiles = {(i // 128, j // 128) for i, j in sel}
+    assert report_key(orep) == [g for g in got if (g[0], g[1]) in sel_tiles]
+    ntm = -(-w.M // 128)
+    for (i, j) in sel:
+        tm, tn = i // 128, j // 128
+        r0, r1 = tm * 128, min(w.M, tm * 128 + 128)
+        c0, c1 = tn * 128, min(w.N, tn * 128 + 128)
+        sub_w = w
+        ab = None
+        # elementwise tolerance on the whole tile
+        opA = d["A"] if w.transA == "N" else d["A"].T
+        opB = d["B"] if w.transB == "N" else d["B"].T
+        ab = np.abs(opA[r0:r1, :]) @ np.abs(opB[:, c0:c1])
+        cc = np.abs(d["C"][r0:r1, c0:c1]) if w.beta != 0 else 0.0
+        tol = gemm_bound(w.K, w.alpha, w.beta, ab, cc)
+        assert (np.abs(C_gpu[r0:r1, c0:c1] - C_or[r0:r1, c0:c1]) <= tol).all()
+        assert (np.abs(C_gpu[r0:r1, c0:c1] - C_clean[r0:r1, c0:c1]) <= 2 * tol).all()
+    sampled_check(w, d, C_gpu, n=100, seed=1, extra=list(zip(plan[0].tolist(), plan[1].tolist()))[:50])
+
+
+def test_config1_4096_tn(ft):
+    check_full_config(ft, syn.CONFIGS[1], oracle_tiles=100)
+
+
+def test_config2_rank_k_update(ft):
+    check_full_config(ft, syn.CONFIGS[2], oracle_tiles=32)
+
+
+def test_config3_16384(ft):
+    check_full_config(ft, syn.CONFIGS[3], oracle_tiles=6)
