@@ -212,7 +212,7 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
     g.M = M; g.N = N; g.K = K; g.alpha = alpha; g.beta = beta;
     const bool va = vec_ok(A, lda), vb = vec_ok(B, ldb);
     if (ft) {
-        const long long Kp = std::max<long long>(16, (K + 15) / 16 * 16);
+        const long long Kp = std::max<long long>(BK, (K + BK - 1) / BK * BK);
         // k-chunks of the encode pass: enough blocks to fill the GPU, chunks >= 32 columns
         int kch = (int)std::max<long long>(1, std::min<long long>(16, (2 * 148 + ntm + ntn - 1) / (ntm + ntn)));
         kch = (int)std::min<long long>(kch, std::max<long long>(1, Kp / 32));

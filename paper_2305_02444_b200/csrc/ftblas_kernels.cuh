@@ -21,10 +21,12 @@
 
 namespace ftb {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4, NTHREADS = 256;
+constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3, NTHREADS = 256;
 constexpr int WM = 64, WN = 32, FM = WM / 8, FN = WN / 8;
-constexpr int LD_MN = 128 + 8;  // doubles per k-row when the mn index is contiguous
-constexpr int LD_K = BK + 4;    // doubles per mn-row when k is contiguous
+// Padded smem strides chosen so that a DMMA fragment load (a half-warp reads 4 mn x 4 k
+// doubles) touches 16 distinct 8-byte bank pairs: row strides == 32 (mod 128) bytes.
+constexpr int LD_MN = 128 + 4;  // doubles per k-row when the mn index is contiguous (1056 B)
+constexpr int LD_K = BK + 4;    // doubles per mn-row when k is contiguous (288 B)
 constexpr double U_ROUND = 1.0 / 9007199254740992.0;  // 2^-53
 
 // smem doubles of one operand tile (one stage)
@@ -109,7 +111,7 @@ __device__ __forceinline__ void load_tile(double *s, const double *X, long long 
         for (int q = 0; q < (128 * BK / 2) / NTHREADS; q++) {
             int c = tid + q * NTHREADS;
             int mn, k;
-            if (KC) { mn = c >> 3; k = (c & 7) * 2; }
+            if (KC) { mn = c / (BK / 2); k = (c % (BK / 2)) * 2; }
             else    { k = c >> 6;  mn = (c & 63) * 2; }
             long long gmn = mn0 + mn, gk = k0 + k;
             int nvalid;
@@ -123,7 +125,7 @@ __device__ __forceinline__ void load_tile(double *s, const double *X, long long 
         for (int q = 0; q < (128 * BK) / NTHREADS; q++) {
             int c = tid + q * NTHREADS;
             int mn, k;
-            if (KC) { mn = c >> 4; k = c & 15; }
+            if (KC) { mn = c / BK; k = c % BK; }
             else    { k = c >> 7;  mn = c & 127; }
             long long gmn = mn0 + mn, gk = k0 + k;
             bool ok = gmn < MNd && gk < Kd;
@@ -228,7 +230,7 @@ __global__ void __launch_bounds__(NTHREADS) encode_kernel(EncodeArgs a) {
 
 
 // ------------------------------------------------------------------ GEMM kernel
-constexpr int LDT = 132;  // epilogue tile leading dimension (2-wavefront fragment stores)
+constexpr int LDT = 130;  // epilogue tile leading dimension (conflict-free fragment stores)
 constexpr int EPI_EL = 128 * LDT   /* tile */
                      + 6 * 128     /* rowS[2][128], rowC[2][128], rowCA[2][128] */
                      + 3 * 128     /* colS, colC, colCA */
@@ -298,8 +300,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(GemmArgs g) {
         load_tile<KCA, VECA>(sA(st), g.A, g.lda, m0, k0, g.M, g.K, tid);
         load_tile<KCB, VECB>(sB(st), g.B, g.ldb, n0, k0, g.N, g.K, tid);
         if (FT) {
-            if (tid < 8)       cp_async16(sW(st) + tid * 2, g.WB + tn * g.Kp + k0 + tid * 2, 16);
-            else if (tid < 16) cp_async16(sV(st) + (tid - 8) * 2, g.VA + tm * g.Kp + k0 + (tid - 8) * 2, 16);
+            if (tid < BK / 2)  cp_async16(sW(st) + tid * 2, g.WB + tn * g.Kp + k0 + tid * 2, 16);
+            else if (tid < BK) cp_async16(sV(st) + (tid - BK / 2) * 2, g.VA + tm * g.Kp + k0 + (tid - BK / 2) * 2, 16);
         }
     };
 
@@ -344,11 +346,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(GemmArgs g) {
             if (!KCA) {
                 const int r = tid & 127, h = tid >> 7;
 #pragma unroll
-                for (int q = 0; q < 8; q++) rp0 = fma(a_s[Tile<KCA>::idx(r, h * 8 + q)], w_s[h * 8 + q], rp0);
+                for (int q = 0; q < BK / 2; q++)
+                    rp0 = fma(a_s[Tile<KCA>::idx(r, h * (BK / 2) + q)], w_s[h * (BK / 2) + q], rp0);
             } else {
                 const int r = warp * 16 + (lane >> 2), kk = lane & 3;
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
+                for (int q = 0; q < BK / 4; q++) {
                     rp0 = fma(a_s[Tile<KCA>::idx(r, kk + 4 * q)], w_s[kk + 4 * q], rp0);
                     rp1 = fma(a_s[Tile<KCA>::idx(r + 8, kk + 4 * q)], w_s[kk + 4 * q], rp1);
                 }
@@ -356,11 +359,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(GemmArgs g) {
             if (!KCB) {
                 const int c = tid & 127, h = tid >> 7;
 #pragma unroll
-                for (int q = 0; q < 8; q++) sp0 = fma(v_s[h * 8 + q], b_s[Tile<KCB>::idx(c, h * 8 + q)], sp0);
+                for (int q = 0; q < BK / 2; q++)
+                    sp0 = fma(v_s[h * (BK / 2) + q], b_s[Tile<KCB>::idx(c, h * (BK / 2) + q)], sp0);
             } else {
                 const int c = warp * 16 + (lane >> 2), kk = lane & 3;
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
+                for (int q = 0; q < BK / 4; q++) {
                     sp0 = fma(v_s[kk + 4 * q], b_s[Tile<KCB>::idx(c, kk + 4 * q)], sp0);
                     sp1 = fma(v_s[kk + 4 * q], b_s[Tile<KCB>::idx(c + 8, kk + 4 * q)], sp1);
                 }

@@ -104,8 +104,16 @@ def make_inputs(w: Workload, *, pad: int = 0, dist: str | None = None) -> dict:
 
 
 def base_of(x: np.ndarray) -> np.ndarray:
-    """The full leading-dimension buffer behind a padded column-major view."""
-    return x if x.base is None else x.base
+    """The full (ld x cols) column-major buffer behind a (possibly padded) matrix view."""
+    own = x.base
+    if own is None or x.ndim != 2:
+        return x
+    ld = x.strides[1] // 8 if x.shape[1] > 1 else x.shape[0]
+    if own.ndim == 1 and ld > 0 and own.size == ld * x.shape[1]:
+        return own.reshape((ld, x.shape[1]), order="F")
+    if own.ndim == 2 and own.shape[1] == x.shape[1]:
+        return own
+    return x
 
 
 def fault_plan(M: int, N: int, n: int, seed: int, *, tile_m: int = TILE_M, tile_n: int = TILE_N,

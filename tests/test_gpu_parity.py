@@ -49,7 +49,6 @@ def run_gpu(ft, w, d, *, plan=None, noft=False, offsets=(0, 0, 0)):
 
 
 def run_oracle(w, d, plan=None, tiles_only=None):
-    C = np.array(syn.base_of(d["C"]), order="F", copy=True)[: w.M, :]
     Cb = np.asfortranarray(syn.base_of(d["C"]).copy())
     Cv = Cb[: w.M, :]
     rep, st = oracle.abft_dgemm(w.transA, w.transB, w.M, w.N, w.K, w.alpha, d["A"], d["lda"],
