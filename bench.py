@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""bench.py -- ABFT DGEMM (FP64, Huang-Abraham checksums fused) throughput on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one full hot-path pass over the workload: the checksum-encode kernel, the
+DMMA GEMM kernel with fused checksum accumulation and the verify/locate/correct
+epilogue, with the workload's seeded bit flips injected (and, for N > 1, the NCCL
+broadcast of op(B) to the row-block shards).  Prints ONE JSON line on rank 0.
+Launch for N > 1:  python -m torch.distributed.run --nproc-per-node N --master-addr
+127.0.0.1 --master-port P bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synthetic as syn  # noqa: E402
+
+METRIC = "ABFT DGEMM FP64 TFLOP/s at 1/2/4/8 B200; FT overhead % vs non-FT; % FP64 peak"
+DEFAULT_WORKLOAD = "c3_16384_sharded"
+# FP64 DMMA peak of B200: 148 SMs x 64 FP64 FMA/clk/SM (DMMA.8x8x4 = 256 FMA per 4 clk per SM)
+# x 2 FLOP x 1.965 GHz max SM clock = 37.23 TFLOP/s; the DMMA microbenchmark reached 37.15
+# (profiles/r01_fp64_pipes.txt).  See DESIGN.md section 5 for why this, not bf16 x ratio.
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.proc, self.lines = gpu, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax.append(float(p[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- helpers
+def col_major_rows(x: np.ndarray, r0: int, r1: int) -> np.ndarray:
+    return np.asfortranarray(x[r0:r1, :])
+
+
+def flat_f(x: np.ndarray) -> np.ndarray:
+    return np.asfortranarray(x).reshape(-1, order="F")
+
+
+def oracle_sample(w, d, plan, seconds: float, first_tile_faulty: bool = True):
+    """Time the CPU oracle (single thread) on whole verification tiles until `seconds`."""
+    import oracle
+    ntm, ntn = -(-w.M // 128), -(-w.N // 128)
+    faulty = sorted({(int(j) // 128) * ntm + int(i) // 128 for i, j in zip(plan[0], plan[1])})
+    rng = np.random.default_rng(12345)
+    order = faulty[:2] + [int(t) for t in rng.permutation(ntm * ntn)[:64]]
+    C = np.asfortranarray(d["C"].copy())
+    done, flops, nf = 0, 0.0, 0
+    t0 = time.perf_counter()
+    for t in order:
+        mask = np.zeros(ntm * ntn, np.uint8)
+        mask[t] = 1
+        oracle.abft_dgemm(w.transA, w.transB, w.M, w.N, w.K, w.alpha, d["A"], d["lda"], d["B"],
+                          d["ldb"], w.beta, C, w.M, faults=plan, tiles_only=mask)
+        tm, tn = t % ntm, t // ntm
+        m = min(128, w.M - tm * 128)
+        n = min(128, w.N - tn * 128)
+        flops += 2.0 * m * n * w.K
+        done += 1
+        nf += t in faulty
+        if time.perf_counter() - t0 >= seconds:
+            break
+    el = time.perf_counter() - t0
+    return {"value": flops / el / 1e12, "unit": "TFLOP/s", "cores": 1, "kind": "oracle",
+            "sample": f"{done} of {ntm * ntn} verification tiles (128x128, K={w.K}) of {w.name}, "
+                      f"{nf} with injected flips; oracle/ftblas_oracle.c single-threaded, "
+                      f"{el:.1f} s"}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, w):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    log(f"[reference] generating {w.name} inputs")
+    d = syn.make_inputs(w)
+    plan = syn.fault_plan(w.M, w.N, w.n_flips, w.seed)
+    step_s = max(1.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(w, d, plan, step_s / 4)
+    vals = []
+    for _ in range(args.steps):
+        vals.append(oracle_sample(w, d, plan, step_s))
+    v = statistics.median(x["value"] for x in vals)
+    cb = dict(vals[-1])
+    cb["value"] = v
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "ms_per_step": 1e3 * step_s,
+           "config": {"workload": w.name, "M": w.M, "N": w.N, "K": w.K, "transA": w.transA,
+                      "transB": w.transB, "alpha": w.alpha, "beta": w.beta, "dist": w.dist,
+                      "seed": w.seed, "injected_flips": w.n_flips},
+           "cpu_baseline": cb,
+           "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=list(syn.CONFIG_BY_NAME))
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    w = syn.CONFIG_BY_NAME[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, w)
+    args.warmup = max(3, args.warmup)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2305_02444_b200 import ftblas as fb
+    from paper_2305_02444_b200 import shard
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    fb.ftblas_set_stream(stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # ---------------------------------------------------------------- inputs
+    t0 = time.perf_counter()
+    d = syn.make_inputs(w)
+    plan = syn.fault_plan(w.M, w.N, w.n_flips, w.seed)
+    r0, r1 = shard.shard_rows(w.M, world, rank)
+    m = r1 - r0
+    if w.transA == "N":
+        A_loc = col_major_rows(d["A"], r0, r1)
+        lda = max(1, m)
+    else:
+        A_loc = np.asfortranarray(d["A"][:, r0:r1])
+        lda = d["lda"]
+    C_loc = col_major_rows(d["C"], r0, r1)
+    ldc = max(1, m)
+    plan_loc = shard.shard_plan(plan, r0, r1)
+    A_dev = torch.from_numpy(flat_f(A_loc)).cuda()
+    B_dev = (torch.from_numpy(flat_f(d["B"])).cuda() if rank == 0
+             else torch.empty(d["B"].size, dtype=torch.float64, device="cuda"))
+    C0_dev = torch.from_numpy(flat_f(C_loc)).cuda()
+    C_dev = C0_dev.clone()
+    log(f"[rank {rank}] inputs ready in {time.perf_counter() - t0:.1f} s; rows [{r0},{r1})")
+    flops_total = 2.0 * w.M * w.N * w.K
+    flops_local = 2.0 * m * w.N * w.K
+
+    def gemm_ft(ta, tb, M_, N_, K_, al, A_, lda_, B_, ldb_, be, C_, ldc_, rep):
+        fb.ftblas_dgemm(ta, tb, M_, N_, K_, al, A_, lda_, B_, ldb_, be, C_, ldc_, rep)
+
+    def gemm_noft(ta, tb, M_, N_, K_, al, A_, lda_, B_, ldb_, be, C_, ldc_, rep):
+        fb.ftblas_dgemm_noft(ta, tb, M_, N_, K_, al, A_, lda_, B_, ldb_, be, C_, ldc_)
+
+    def step(gemm, broadcast):
+        if w.beta != 0.0:
+            pass  # C := alpha AB + beta C accumulates into C; the value drifts but the work is identical
+        shard.sharded_dgemm(gemm, w.transA, w.transB, w.M, w.N, w.K, w.alpha, A_dev, lda, B_dev,
+                            d["ldb"], w.beta, C_dev, ldc, rank=rank, world=world,
+                            broadcast=broadcast and world > 1)
+
+    def timed(fn, steps):
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1)) / steps
+
+    K, W = args.steps, args.warmup
+    if plan_loc is not None and len(plan_loc[0]):
+        fb.ftblas_set_fault_plan(*plan_loc)
+    else:
+        fb.ftblas_clear_fault_plan()
+    for _ in range(W):
+        step(gemm_ft, True)
+    torch.cuda.synchronize()
+
+    # ---------------------------------------------------------------- headline: FT + flips
+    clk = ClockSampler(local)
+    with clk:
+        time.sleep(0.4)
+        fb.ftblas_profile(True)
+        fb.ftblas_profile_read()
+        n0 = fb.ftblas_launch_count()
+        ms_step = timed(lambda: step(gemm_ft, True), K)
+        launches = fb.ftblas_launch_count() - n0
+        fb.ftblas_profile(False)
+        enc_ms, gemm_ms, n_g = fb.ftblas_profile_read()
+        rep = fb.ftblas_report_fetch(fb.Report(max(16, 2 * len(plan_loc[0]))))
+        # overhead comparisons on the local GEMM call (no broadcast), same inputs
+        ms_ft_err = timed(lambda: step(gemm_ft, False), K)
+        fb.ftblas_clear_fault_plan()
+        ms_ft0 = timed(lambda: step(gemm_ft, False), K)
+        ms_noft = timed(lambda: step(gemm_noft, False), K)
+        for _ in range(2):  # keep the GPU loaded until the sampler stops
+            step(gemm_ft, False)
+        torch.cuda.synchronize()
+    clocks = clk.summary()
+    planned_local = len(plan_loc[0])
+    entries = shard.globalize(rep.entries(), r0)
+    located = sorted((e["i"], e["j"]) for e in entries)
+    want = sorted(zip((plan_loc[0] + r0).tolist(), plan_loc[1].tolist()))
+    ok_local = (rep.count == planned_local) and located == want
+    ok_all = sum_over_ranks(0.0 if ok_local else 1.0) == 0.0
+    reported = int(sum_over_ranks(float(rep.count)))
+    launches_all = int(sum_over_ranks(float(launches)))
+    gemm_avg_ms = gemm_ms / max(1, n_g)
+    enc_avg_ms = enc_ms / max(1, n_g)
+
+    # ---------------------------------------------------------------- e2e: host buffers
+    e2e = None
+    if not args.skip_e2e:
+        if plan_loc is not None and len(plan_loc[0]):
+            fb.ftblas_set_fault_plan(*plan_loc)
+
+        def pinned(x: np.ndarray):
+            t = torch.empty(x.size, dtype=torch.float64, pin_memory=True)
+            t.numpy()[:] = flat_f(x)
+            return t
+
+        hA, hB, hC = pinned(A_loc), pinned(d["B"]), pinned(C_loc)
+        h2d = A_loc.nbytes + d["B"].nbytes + (C_loc.nbytes if w.beta != 0.0 else 0)
+        d2h = C_loc.nbytes
+
+        def e2e_step():
+            fb.ftblas_dgemm_host(w.transA, w.transB, m, w.N, w.K, w.alpha, hA.data_ptr(), lda,
+                                 hB.data_ptr(), d["ldb"], w.beta, hC.data_ptr(), ldc, None)
+
+        e2e_step()
+        ms_e2e = timed(e2e_step, max(2, min(K, 3)))
+        fb.ftblas_clear_fault_plan()
+        e2e = {"value": flops_total / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": int(sum_over_ranks(float(h2d))),
+               "d2h_bytes_per_step": int(sum_over_ranks(float(d2h))),
+               "ms_per_step": ms_e2e,
+               "path": "ftblas_dgemm_host (pinned host A,B,C -> device, ABFT DGEMM, C -> host)"}
+        del hA, hB, hC
+
+    # ---------------------------------------------------------------- traffic (ncu capture)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            key = f"{w.name}/world{world}"
+            if key in tj:
+                traffic = tj[key]["dram_bytes_per_launch"]
+        except (ValueError, KeyError):
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        log("[bench] timing the CPU oracle on a bounded sample")
+        cpu = oracle_sample(w, d, plan, args.cpu_seconds)
+
+    if rank == 0:
+        value = flops_total / (ms_step * 1e-3) / 1e12
+        achieved = flops_local / (gemm_avg_ms * 1e-3) / 1e12
+        tf = lambda ms: flops_total / (ms * 1e-3) / 1e12  # noqa: E731
+        out = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": w.name, "M": w.M, "N": w.N, "K": w.K, "transA": w.transA,
+                       "transB": w.transB, "alpha": w.alpha, "beta": w.beta,
+                       "dist": {"uniform": "U[-1,1]", "normal": "N(0,1)"}[w.dist], "seed": w.seed,
+                       "injected_flips": w.n_flips, "flip_bits": [syn.BIT_LO, syn.BIT_HI],
+                       "verification_tile": [syn.TILE_M, syn.TILE_N],
+                       "parallelism": f"row-block x{world}" + (", op(B) NCCL broadcast per step" if world > 1 else ""),
+                       "l2": "no flush: operands (%.1f GiB) >> 126 MB L2" % ((d["A"].nbytes + d["B"].nbytes + d["C"].nbytes) / 2**30)},
+            "fp64_peak_tflops": FP64_PEAK_TFLOPS,
+            "pct_fp64_peak": 100.0 * value / (FP64_PEAK_TFLOPS * world),
+            "noft_tflops": tf(ms_noft), "ft_0err_tflops": tf(ms_ft0), "ft_flips_tflops": tf(ms_ft_err),
+            "ft_overhead_pct": {"errors_0": 100.0 * (ms_ft0 / ms_noft - 1.0),
+                                f"errors_{w.n_flips}": 100.0 * (ms_ft_err / ms_noft - 1.0)},
+            "corrections": {"planned": int(len(plan[0])), "reported": reported, "all_located_and_corrected": bool(ok_all)},
+            "gpu_launches": launches_all,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                         "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                         "kernel": "gemm_kernel<FT> (DMMA + fused ABFT)", "kernel_ms": gemm_avg_ms,
+                         "encode_kernel_ms": enc_avg_ms,
+                         "peak_source": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DMMA microbench 37.15, profiles/r01_fp64_pipes.txt)"},
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -118,6 +118,16 @@ int ftblas_set_stream(void *stream);
 /* Number of kernels the library launched since load (for launch accounting). */
 int64_t ftblas_launch_count(void);
 
+/* Per-kernel device timing (for roofline accounting in bench.py).  enable != 0:
+ * subsequent ftblas_dgemm / ftblas_dgemm_noft calls record CUDA events on the
+ * library stream around each kernel launch; enable == 0 stops recording.
+ * ftblas_profile_read synchronizes, returns the summed device milliseconds of
+ * the encode kernel and of the GEMM kernel and the number of GEMM launches
+ * recorded since the last read, and clears the record.  Any output pointer may
+ * be NULL. */
+int ftblas_profile(int enable);
+int ftblas_profile_read(double *encode_ms, double *gemm_ms, int64_t *gemm_launches);
+
 /* Verification tile shape (FTBLAS_TILE_M, FTBLAS_TILE_N). */
 void ftblas_tile_shape(int32_t *tile_m, int32_t *tile_n);
 

@@ -50,6 +50,9 @@ struct Ctx {
     std::vector<int> plan_bit;
     DevBuf hA, hB, hC;    // ftblas_dgemm_host device staging
     long long launches = 0;
+    bool profiling = false;
+    struct Rec { cudaEvent_t e0, e1, e2; bool ft; };
+    std::vector<Rec> recs, pool;
     char err[512] = "no error";
     int device = -1;
 };
@@ -175,6 +178,20 @@ int prepare_plan(long long M, long long N, GemmArgs &g) {
     return 0;
 }
 
+cudaEvent_t new_event() {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+Ctx::Rec take_rec(bool ft) {
+    Ctx &c = ctx();
+    Ctx::Rec r;
+    if (!c.pool.empty()) { r = c.pool.back(); c.pool.pop_back(); }
+    else { r.e0 = new_event(); r.e1 = new_event(); r.e2 = new_event(); }
+    r.ft = ft;
+    return r;
+}
+
 int fetch_report(ftblas_err_report *r) {
     Ctx &c = ctx();
     CK(cudaStreamSynchronize(c.stream), "report sync");
@@ -211,6 +228,11 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
     g.A = A; g.B = B; g.C = C; g.lda = lda; g.ldb = ldb; g.ldc = ldc;
     g.M = M; g.N = N; g.K = K; g.alpha = alpha; g.beta = beta;
     const bool va = vec_ok(A, lda), vb = vec_ok(B, ldb);
+    Ctx::Rec rec{};
+    if (c.profiling) {
+        rec = take_rec(ft);
+        CK(cudaEventRecord(rec.e0, c.stream), "event");
+    }
     if (ft) {
         const long long Kp = std::max<long long>(BK, (K + BK - 1) / BK * BK);
         // k-chunks of the encode pass: enough blocks to fill the GPU, chunks >= 32 columns
@@ -239,9 +261,15 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
         encode_kernel<<<grid, NTHREADS, 0, c.stream>>>(ea);
         c.launches++;
         CK(cudaGetLastError(), "encode_kernel launch");
+        if (c.profiling) CK(cudaEventRecord(rec.e1, c.stream), "event");
         CK(launch_gemm<true>(kca, kcb, va, vb, g, ntm * ntn, c.stream), "gemm_kernel<FT> launch");
     } else {
+        if (c.profiling) CK(cudaEventRecord(rec.e1, c.stream), "event");
         CK(launch_gemm<false>(kca, kcb, va, vb, g, ntm * ntn, c.stream), "gemm_kernel launch");
+    }
+    if (c.profiling) {
+        CK(cudaEventRecord(rec.e2, c.stream), "event");
+        c.recs.push_back(rec);
     }
     if (rep) return fetch_report(rep);
     return 0;
@@ -319,6 +347,30 @@ int ftblas_set_stream(void *stream) {
 }
 
 int64_t ftblas_launch_count(void) { return ctx().launches; }
+
+int ftblas_profile(int enable) {
+    ctx().profiling = enable != 0;
+    return 0;
+}
+
+int ftblas_profile_read(double *encode_ms, double *gemm_ms, int64_t *gemm_launches) {
+    Ctx &c = ctx();
+    double enc = 0.0, gem = 0.0;
+    for (auto &r : c.recs) {
+        CK(cudaEventSynchronize(r.e2), "event sync");
+        float a = 0.f, b = 0.f;
+        CK(cudaEventElapsedTime(&a, r.e0, r.e1), "elapsed");
+        CK(cudaEventElapsedTime(&b, r.e1, r.e2), "elapsed");
+        enc += a;
+        gem += b;
+    }
+    if (encode_ms) *encode_ms = enc;
+    if (gemm_ms) *gemm_ms = gem;
+    if (gemm_launches) *gemm_launches = (int64_t)c.recs.size();
+    for (auto &r : c.recs) c.pool.push_back(r);
+    c.recs.clear();
+    return 0;
+}
 
 void ftblas_tile_shape(int32_t *tile_m, int32_t *tile_n) {
     if (tile_m) *tile_m = FTBLAS_TILE_M;

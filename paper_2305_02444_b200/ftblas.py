@@ -55,6 +55,11 @@ def _load():
     L.ftblas_set_stream.restype = ct.c_int
     L.ftblas_launch_count.argtypes = []
     L.ftblas_launch_count.restype = I
+    L.ftblas_profile.argtypes = [ct.c_int]
+    L.ftblas_profile.restype = ct.c_int
+    L.ftblas_profile_read.argtypes = [ct.POINTER(ct.c_double), ct.POINTER(ct.c_double),
+                                      ct.POINTER(ct.c_int64)]
+    L.ftblas_profile_read.restype = ct.c_int
     L.ftblas_tile_shape.argtypes = [ct.POINTER(ct.c_int32), ct.POINTER(ct.c_int32)]
     L.ftblas_tile_shape.restype = None
     L.ftblas_last_error.argtypes = []
@@ -69,7 +74,8 @@ lib = _load()
 # Symbols include/ftblas.h declares (checked by tests/test_abi.py).
 EXPORTS = ("ftblas_dgemm", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_report_fetch",
            "ftblas_set_fault_plan", "ftblas_set_stream", "ftblas_launch_count",
-           "ftblas_tile_shape", "ftblas_last_error", "ftblas_release")
+           "ftblas_tile_shape", "ftblas_last_error", "ftblas_release", "ftblas_profile",
+           "ftblas_profile_read")
 
 
 def _ptr(x):
@@ -170,6 +176,17 @@ def ftblas_set_stream(stream):
 
 def ftblas_launch_count() -> int:
     return lib.ftblas_launch_count()
+
+
+def ftblas_profile(enable: bool):
+    _check(lib.ftblas_profile(1 if enable else 0))
+
+
+def ftblas_profile_read():
+    """(encode_ms, gemm_ms, gemm_launches) recorded since the last read."""
+    a, b, n = ct.c_double(), ct.c_double(), ct.c_int64()
+    _check(lib.ftblas_profile_read(ct.byref(a), ct.byref(b), ct.byref(n)))
+    return a.value, b.value, n.value
 
 
 def ftblas_tile_shape():

@@ -150,15 +150,3 @@ def fault_plan(M: int, N: int, n: int, seed: int, *, tile_m: int = TILE_M, tile_
     return (np.array([out_i[q] for q in order], dtype=np.int64),
             np.array([out_j[q] for q in order], dtype=np.int64),
             np.array([out_b[q] for q in order], dtype=np.int32))
-
-
-def shard_rows(M: int, world: int, rank: int, align: int = TILE_M) -> tuple:
-    """Row range [r0, r1) of C (and op(A)) owned by ``rank`` in a row-block shard.
-
-    Blocks are multiples of ``align`` rows (whole verification tiles) except the last.
-    """
-    tiles = -(-M // align)
-    per, rem = divmod(tiles, world)
-    t0 = rank * per + min(rank, rem)
-    t1 = t0 + per + (1 if rank < rem else 0)
-    return min(M, t0 * align), min(M, t1 * align)
