@@ -105,7 +105,7 @@ cudaError_t launch_gemm_t(const GemmArgs &g, long long tiles, cudaStream_t s) {
     const int bytes = SmemPlan<KCA, KCB, FT>::BYTES;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)tiles, NTHREADS, bytes, s>>>(g);
+    kern<<<(unsigned)tiles, GEMM_THREADS, bytes, s>>>(g);
     ctx().launches++;
     return cudaGetLastError();
 }

@@ -84,6 +84,29 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// mbarrier primitives (producer/consumer pipeline between the load warp and the MMA warps)
+__device__ __forceinline__ void mbar_init(unsigned long long *b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *b) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(smem_u32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *b, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tLAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra LAB_WAIT;\n\t}\n" ::"r"(smem_u32(b)), "r"(parity)
+        : "memory");
+}
+// arrive on b when all prior cp.async of this thread have landed (count pre-set at init)
+__device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long *b) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_mma() {  // named barrier over the NTHREADS MMA threads only
+    asm volatile("bar.sync 1, %0;\n" ::"n"(NTHREADS) : "memory");
+}
+
 __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1)
@@ -103,13 +126,13 @@ __device__ __forceinline__ const double *gaddr(const double *X, long long ld, lo
 }
 
 // Stage one 128 x BK operand tile into smem with cp.async (zero-fill outside [0,MNd) x [0,Kd)).
-template <bool KC, bool VEC>
+template <bool KC, bool VEC, int NT = NTHREADS>
 __device__ __forceinline__ void load_tile(double *s, const double *X, long long ld, long long mn0,
                                           long long k0, long long MNd, long long Kd, int tid) {
     if (VEC) {  // 16-byte chunks along the contiguous dimension (needs 16B-aligned X, even ld)
 #pragma unroll
-        for (int q = 0; q < (128 * BK / 2) / NTHREADS; q++) {
-            int c = tid + q * NTHREADS;
+        for (int q = 0; q < (128 * BK / 2) / NT; q++) {
+            int c = tid + q * NT;
             int mn, k;
             if (KC) { mn = c / (BK / 2); k = (c % (BK / 2)) * 2; }
             else    { k = c >> 6;  mn = (c & 63) * 2; }
@@ -122,13 +145,59 @@ __device__ __forceinline__ void load_tile(double *s, const double *X, long long 
         }
     } else {  // 8-byte elements: any alignment / odd ld
 #pragma unroll
-        for (int q = 0; q < (128 * BK) / NTHREADS; q++) {
-            int c = tid + q * NTHREADS;
+        for (int q = 0; q < (128 * BK) / NT; q++) {
+            int c = tid + q * NT;
             int mn, k;
             if (KC) { mn = c / BK; k = c % BK; }
             else    { k = c >> 7;  mn = c & 127; }
             long long gmn = mn0 + mn, gk = k0 + k;
             bool ok = gmn < MNd && gk < Kd;
+            cp_async8(s + Tile<KC>::idx(mn, k), ok ? gaddr<KC>(X, ld, gmn, gk) : X, ok ? 8 : 0);
+        }
+    }
+}
+
+// Producer-side staging of one 128 x BK operand tile by the PRODUCER_THREADS threads of the
+// load warpgroup: one base pointer + a constant stride per thread (low register footprint,
+// the producer runs with PRODUCER_REGS registers after setmaxnreg.dec).
+constexpr int PRODUCER_THREADS_ = 128;
+template <bool KC, bool VEC>
+__device__ __forceinline__ void produce_tile(double *s, const double *X, long long ld, long long mn0,
+                                             long long k0, long long MNd, long long Kd, int pt) {
+    if (VEC) {
+        if (KC) {  // k contiguous: BK/2 16-byte chunks per mn row
+            constexpr int CPR = BK / 2, STEP = PRODUCER_THREADS_ / CPR;
+            const int k = (pt % CPR) * 2, mnb = pt / CPR;
+            const long long gk = k0 + k;
+            const int kval = (int)min(2ll, max(0ll, Kd - gk));
+            const double *src = X + gk + (mn0 + mnb) * ld;
+            double *dst = s + mnb * LD_K + k;
+#pragma unroll 4
+            for (int q = 0; q < 128 / STEP; q++) {
+                const int nv = (mn0 + mnb + q * STEP < MNd) ? kval : 0;
+                cp_async16(dst + q * STEP * LD_K, nv ? src + (long long)q * STEP * ld : X, nv * 8);
+            }
+        } else {   // mn contiguous: 64 chunks per k row
+            constexpr int STEP = PRODUCER_THREADS_ / 64;
+            const int mn = (pt % 64) * 2, kb = pt / 64;
+            const long long gmn = mn0 + mn;
+            const int mval = (int)min(2ll, max(0ll, MNd - gmn));
+            const double *src = X + gmn + (k0 + kb) * ld;
+            double *dst = s + kb * LD_MN + mn;
+#pragma unroll 4
+            for (int q = 0; q < BK / STEP; q++) {
+                const int nv = (k0 + kb + q * STEP < Kd) ? mval : 0;
+                cp_async16(dst + q * STEP * LD_MN, nv ? src + (long long)q * STEP * ld : X, nv * 8);
+            }
+        }
+    } else {  // 8-byte elements (misaligned pointer / odd ld): correctness path
+#pragma unroll 1
+        for (int c = pt; c < 128 * BK; c += PRODUCER_THREADS_) {
+            int mn, k;
+            if (KC) { mn = c / BK; k = c % BK; }
+            else    { k = c >> 7;  mn = c & 127; }
+            const long long gmn = mn0 + mn, gk = k0 + k;
+            const bool ok = gmn < MNd && gk < Kd;
             cp_async8(s + Tile<KC>::idx(mn, k), ok ? gaddr<KC>(X, ld, gmn, gk) : X, ok ? 8 : 0);
         }
     }
@@ -277,9 +346,17 @@ __device__ void warp_recompute(const GemmArgs &g, long long i, long long j, doub
     }
 }
 
+// Block = NTHREADS MMA threads (8 warps) + 1 producer warp that stages tiles with cp.async
+// and signals per-stage `full` mbarriers; MMA warps release stages through `empty` mbarriers
+// (no CTA-wide barrier in the mainloop, so the two MMA warps of an SMSP drift independently).
+constexpr int PRODUCER_THREADS = PRODUCER_THREADS_;  // one warpgroup; registers go to the MMA warps
+constexpr int GEMM_THREADS = NTHREADS + PRODUCER_THREADS;
+constexpr int MMA_REGS = 224, PRODUCER_REGS = 64;  // 2x128x224 + 128x64 = 64K registers
+
 template <bool KCA, bool KCB, bool VECA, bool VECB, bool FT>
-__global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(GemmArgs g) {
+__global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmArgs g) {
     extern __shared__ __align__(128) double smem[];
+    __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
     using SP = SmemPlan<KCA, KCB, FT>;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp & 1, wn = warp >> 1;
@@ -294,16 +371,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(GemmArgs g) {
     auto sW = [&](int st) { return smem + st * SP::STAGE_EL + SP::A_EL + SP::B_EL; };
     auto sV = [&](int st) { return smem + st * SP::STAGE_EL + SP::A_EL + SP::B_EL + BK; };
 
-    auto issue = [&](int kt) {
-        const int st = kt % STAGES;
-        const long long k0 = (long long)kt * BK;
-        load_tile<KCA, VECA>(sA(st), g.A, g.lda, m0, k0, g.M, g.K, tid);
-        load_tile<KCB, VECB>(sB(st), g.B, g.ldb, n0, k0, g.N, g.K, tid);
-        if (FT) {
-            if (tid < BK / 2)  cp_async16(sW(st) + tid * 2, g.WB + tn * g.Kp + k0 + tid * 2, 16);
-            else if (tid < BK) cp_async16(sV(st) + (tid - BK / 2) * 2, g.VA + tm * g.Kp + k0 + (tid - BK / 2) * 2, 16);
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&full_bar[s], PRODUCER_THREADS); // one cp.async arrival per producer thread
+            mbar_init(&empty_bar[s], NTHREADS / 32);   // one arrival per MMA warp
         }
-    };
+    }
+    __syncthreads();
+
+    if (warp >= NTHREADS / 32) {
+        // ------------------------------------------------------------ producer warpgroup
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
+        const int pt = tid - NTHREADS;
+        for (int kt = 0; kt < ktiles; kt++) {
+            const int st = kt % STAGES;
+            if (kt >= STAGES) mbar_wait(&empty_bar[st], ((kt / STAGES) - 1) & 1);
+            const long long k0 = (long long)kt * BK;
+            produce_tile<KCA, VECA>(sA(st), g.A, g.lda, m0, k0, g.M, g.K, pt);
+            produce_tile<KCB, VECB>(sB(st), g.B, g.ldb, n0, k0, g.N, g.K, pt);
+            if (FT) {
+#pragma unroll
+                for (int q = pt; q < BK; q += PRODUCER_THREADS) {
+                    if (q < BK / 2) cp_async16(sW(st) + q * 2, g.WB + tn * g.Kp + k0 + q * 2, 16);
+                    else            cp_async16(sV(st) + (q - BK / 2) * 2, g.VA + tm * g.Kp + k0 + (q - BK / 2) * 2, 16);
+                }
+            }
+            cp_async_mbar_arrive(&full_bar[st]);
+        }
+        cp_wait<0>();
+        return;
+    }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(MMA_REGS));
 
     double acc[FM][FN][2];
 #pragma unroll
@@ -315,17 +413,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(GemmArgs g) {
     // 16w+r and 16w+8+r at k = kk, kk+4, kk+8, kk+12 (2-wavefront smem reads).
     double rp0 = 0.0, rp1 = 0.0, sp0 = 0.0, sp1 = 0.0;
 
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; s++) {
-        if (s < ktiles) issue(s);
-        cp_commit();
-    }
     for (int kt = 0; kt < ktiles; kt++) {
-        cp_wait<STAGES - 2>();
-        __syncthreads();
-        if (kt + STAGES - 1 < ktiles) issue(kt + STAGES - 1);
-        cp_commit();
         const int st = kt % STAGES;
+        mbar_wait(&full_bar[st], (kt / STAGES) & 1);
         const double *a_s = sA(st), *b_s = sB(st);
 #pragma unroll
         for (int kk = 0; kk < BK / 4; kk++) {
@@ -370,9 +460,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(GemmArgs g) {
                 }
             }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[st]);
     }
-    cp_wait<0>();
-    __syncthreads();
+    bar_mma();  // all MMA warps done with the pipeline smem (the producer has no pending copies)
 
     const bool beta0 = (g.beta == 0.0);
     if (!FT) {
@@ -439,7 +530,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(GemmArgs g) {
             const long long gi = m0 + row, gj = n0 + col;
             tileS[row + col * LDT] = (gi < g.M && gj < g.N) ? g.C[gi + gj * g.ldc] : 0.0;
         }
-        __syncthreads();
+        bar_mma();
         double s = 0.0, sa = 0.0;
         for (int c = hh * 64; c < hh * 64 + 64; c++) {
             const double v = tileS[rr + c * LDT];
@@ -461,7 +552,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(GemmArgs g) {
             }
             if (lane == 0) { colC[c] = cs; colCA[c] = ca; }
         }
-        __syncthreads();
+        bar_mma();
     }
     // fault injection (test harness): flip accumulator bits of planned elements of this tile
     if (g.plan_ptr) {
@@ -495,7 +586,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(GemmArgs g) {
                 else       o = fma(g.alpha, acc[a][b][e], g.beta * tileS[row + col * LDT]);
                 tileS[row + col * LDT] = ok ? o : 0.0;
             }
-    __syncthreads();
+    bar_mma();
     // row / column sums of the computed tile (warp-shuffle reductions for the columns)
     {
         double s = 0.0;
@@ -511,7 +602,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(GemmArgs g) {
             if (lane == 0) colS[c] = cs;
         }
     }
-    __syncthreads();
+    bar_mma();
     // verification: flag rows / columns beyond the round-off threshold
     const double aa = fabs(g.alpha), ab = fabs(g.beta);
     if (tid < 128) {
@@ -558,7 +649,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(GemmArgs g) {
             }
         }
     }
-    __syncthreads();
+    bar_mma();
     const int nr = flags[0], nc = flags[1];
     if (nr != 0 || nc != 0) {
         // ---------------------------------------------------------- locate + correct (rare)
@@ -575,7 +666,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(GemmArgs g) {
                     const int t = flags[130 + y]; flags[130 + y] = flags[130 + y - 1]; flags[130 + y - 1] = t;
                 }
         }
-        __syncthreads();
+        bar_mma();
         const bool single = (nr == 1 && nc == 1);  // Huang-Abraham location (line 540)
         const long long ncr = nr ? nr : mvalid, ncc = nc ? nc : nvalid;
         for (long long q = warp; q < ncr * ncc; q += NTHREADS / 32) {
@@ -600,7 +691,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(GemmArgs g) {
                 }
             }
         }
-        __syncthreads();
+        bar_mma();
     }
     // coalesced store of the verified tile
     for (int idx = tid; idx < BM * BN; idx += NTHREADS) {
