@@ -351,7 +351,14 @@ __device__ void warp_recompute(const GemmArgs &g, long long i, long long j, doub
 // (no CTA-wide barrier in the mainloop, so the two MMA warps of an SMSP drift independently).
 constexpr int PRODUCER_THREADS = PRODUCER_THREADS_;  // one warpgroup; registers go to the MMA warps
 constexpr int GEMM_THREADS = NTHREADS + PRODUCER_THREADS;
-constexpr int MMA_REGS = 224, PRODUCER_REGS = 64;  // 2x128x224 + 128x64 = 64K registers
+// setmaxnreg only moves registers inside the CTA's launch allocation: ptxas caps a
+// __launch_bounds__(384, 1) kernel at 168 registers/thread (65536/384 rounded down to a
+// multiple of 8), so the pool is 384 x 168 = 64512.  An .inc that asks for more than the
+// pool blocks forever.
+constexpr int LAUNCH_REGS = 168;
+constexpr int MMA_REGS = 224, PRODUCER_REGS = 56;  // 256x224 + 128x56 = 64512
+static_assert(NTHREADS * MMA_REGS + PRODUCER_THREADS * PRODUCER_REGS <= GEMM_THREADS * LAUNCH_REGS,
+              "setmaxnreg budget exceeds the launch register allocation (would deadlock)");
 
 template <bool KCA, bool KCB, bool VECA, bool VECB, bool FT>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmArgs g) {
