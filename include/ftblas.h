@@ -9,12 +9,14 @@
  * p[r + c*ld].
  *
  * Fault tolerance (ftblas_dgemm only): Huang-Abraham algorithm-based fault
- * tolerance (section II.A), fused into the GEMM kernel
- * (section V.B): checksums A^c = [A; e^T A] and B^r = [B, B e] are
- * encoded per verification tile (FTBLAS_TILE_M x FTBLAS_TILE_N block of C),
- * the checksum row e^T C and column C e of the product are accumulated in the
- * same mainloop as the MMA, and the epilogue compares them with the computed
- * tile, flags any row/column whose difference "exceeds the round-off
+ * tolerance (section II.A; fusion: section V.B, line
+ * 558): checksums A^c = [A; e^T A] and B^r = [B, B e] are encoded per
+ * verification tile (FTBLAS_TILE_M x FTBLAS_TILE_N block of C), the checksum
+ * row e^T C = (e^T A) B and column C e = A (B e) of the product are formed on
+ * the FP64 tensor cores (ftblas_set_checksum_mode: as two checksum GEMMs
+ * before the main GEMM -- the default -- or accumulated in the same mainloop
+ * as the MMA), and the epilogue of the GEMM kernel compares them with the
+ * computed tile, flags any row/column whose difference "exceeds the round-off
  * threshold" (line 517), locates the erroneous element at the intersection of
  * the flagged row and column (line 540) and corrects it before C is stored.
  * The detection threshold, the multi-flag rule and the correction rule are the
@@ -112,6 +114,22 @@ int ftblas_report_fetch(ftblas_err_report *err_report);
  * against the M x N of each call; entries outside it are ignored. */
 int ftblas_set_fault_plan(int64_t n, const int64_t *i, const int64_t *j, const int32_t *bit);
 
+/* Where the checksum row/column of C (the border of C^f = A^c B^r, PAPER.md
+ * line 516) is computed by subsequent ftblas_dgemm calls:
+ *   FTBLAS_CHECKSUM_GEMM  (default): R = op(A) (B e_J) for every column tile J and
+ *       S = (e_I^T A) op(B) for every row tile I as two DMMA GEMMs (M x ceil(N/128)
+ *       and N x ceil(M/128)) before the main GEMM; the main kernel's mainloop is
+ *       the plain one and its epilogue verifies against R, S.
+ *   FTBLAS_CHECKSUM_FUSED: accumulated in the main kernel's mainloop from the
+ *       operand fragments of the MMA (DFMA next to the DMMA stream).
+ * Both give the same verification, reports and corrections up to rounding of
+ * the checksum (covered by the threshold, R4).  Returns 0, or -1 for
+ * an unknown mode. */
+#define FTBLAS_CHECKSUM_GEMM 0
+#define FTBLAS_CHECKSUM_FUSED 1
+int ftblas_set_checksum_mode(int mode);
+int ftblas_get_checksum_mode(void);
+
 /* Stream for subsequent calls (a cudaStream_t passed as void*; NULL = default stream). */
 int ftblas_set_stream(void *stream);
 
@@ -122,7 +140,8 @@ int64_t ftblas_launch_count(void);
  * subsequent ftblas_dgemm / ftblas_dgemm_noft calls record CUDA events on the
  * library stream around each kernel launch; enable == 0 stops recording.
  * ftblas_profile_read synchronizes, returns the summed device milliseconds of
- * the encode kernel and of the GEMM kernel and the number of GEMM launches
+ * the checksum stage (encode kernel + checksum GEMMs in FTBLAS_CHECKSUM_GEMM
+ * mode) and of the main GEMM kernel and the number of GEMM calls
  * recorded since the last read, and clears the record.  Any output pointer may
  * be NULL. */
 int ftblas_profile(int enable);

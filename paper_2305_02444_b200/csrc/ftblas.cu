@@ -54,6 +54,7 @@ struct Ctx {
     struct Rec { cudaEvent_t e0, e1, e2; bool ft; };
     std::vector<Rec> recs, pool;
     char err[512] = "no error";
+    int checksum_mode = FTBLAS_CHECKSUM_GEMM;
     int device = -1;
 };
 Ctx &ctx() {
@@ -99,27 +100,62 @@ int check_args(char ta, char tb, long long M, long long N, long long K, const vo
     return 0;
 }
 
-template <bool KCA, bool KCB, bool VA, bool VB, bool FT>
-cudaError_t launch_gemm_t(const GemmArgs &g, long long tiles, cudaStream_t s) {
-    auto kern = gemm_kernel<KCA, KCB, VA, VB, FT>;
-    const int bytes = SmemPlan<KCA, KCB, FT>::BYTES;
+template <bool KCA, bool KCB, bool TMA, int MODE>
+cudaError_t launch_gemm_t(const GemmArgs &g, const CUtensorMap &ma, const CUtensorMap &mb, long long tiles,
+                          cudaStream_t s) {
+    auto kern = gemm_kernel<KCA, KCB, TMA, MODE>;
+    const int bytes = SmemPlan<MODE>::BYTES;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)tiles, GEMM_THREADS, bytes, s>>>(g);
+    kern<<<(unsigned)tiles, GEMM_THREADS, bytes, s>>>(g, ma, mb);
     ctx().launches++;
     return cudaGetLastError();
 }
 
-template <bool FT>
-cudaError_t launch_gemm(bool kca, bool kcb, bool va, bool vb, const GemmArgs &g, long long tiles, cudaStream_t s) {
-    // 16 instantiations: transpose layout x 16-byte vector loads
-#define L(a, b, c, d) if (kca == a && kcb == b && va == c && vb == d) return launch_gemm_t<a, b, c, d, FT>(g, tiles, s)
-    L(false, true, true, true); L(false, false, true, true); L(true, true, true, true); L(true, false, true, true);
-    L(false, true, false, true); L(false, false, false, true); L(true, true, false, true); L(true, false, false, true);
-    L(false, true, true, false); L(false, false, true, false); L(true, true, true, false); L(true, false, true, false);
-    L(false, true, false, false); L(false, false, false, false); L(true, true, false, false); L(true, false, false, false);
+template <int MODE>
+cudaError_t launch_gemm(bool kca, bool kcb, bool tma, const GemmArgs &g, const CUtensorMap &ma,
+                        const CUtensorMap &mb, long long tiles, cudaStream_t s) {
+    // 8 instantiations per mode: transpose layout x (TMA | cp.async fallback)
+#define L(a, b, c) if (kca == a && kcb == b && tma == c) return launch_gemm_t<a, b, c, MODE>(g, ma, mb, tiles, s)
+    L(false, true, true); L(false, false, true); L(true, true, true); L(true, false, true);
+    L(false, true, false); L(false, false, false); L(true, true, false); L(true, false, false);
 #undef L
     return cudaErrorInvalidValue;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link)
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// Tensor map of one operand, as gemm_kernel stages it (ftblas_kernels.cuh, Tile): KC=false
+// (mn contiguous): dims {MNd, Kd}, box {16, BK}; KC=true (k contiguous): dims {Kd, MNd}, box
+// {16, 128}.  128-byte swizzle, zero fill out of bounds.  Returns false when TMA cannot
+// describe the operand (the kernel then stages it with cp.async).
+bool make_operand_map(CUtensorMap *m, const double *X, long long ld, long long MNd, long long Kd, bool kc) {
+    std::memset(m, 0, sizeof(*m));
+    EncodeTiledFn fn = encode_tiled();
+    if (!fn || !X || MNd <= 0 || Kd <= 0 || (reinterpret_cast<uintptr_t>(X) & 15) || (ld & 1)) return false;
+    if (MNd >= (1ll << 31) || Kd >= (1ll << 31)) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)(kc ? Kd : MNd), (cuuint64_t)(kc ? MNd : Kd)};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+    const cuuint32_t box[2] = {16u, kc ? 128u : (cuuint32_t)BK};
+    const cuuint32_t estr[2] = {1u, 1u};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(X), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
 }
 
 bool vec_ok(const void *p, long long ld) {
@@ -208,6 +244,79 @@ int fetch_report(ftblas_err_report *r) {
     return 0;
 }
 
+// Operand staging for one GEMM call: tensor maps when both operands can be described by
+// TMA (16-byte aligned, even ld), else the cp.async fallback for both.
+struct Staging {
+    CUtensorMap ma, mb;
+    bool tma;
+};
+Staging make_staging(const double *A, long long lda, long long M, bool kca, const double *B, long long ldb,
+                     long long N, bool kcb, long long K, double alpha) {
+    Staging st;
+    const bool use = K > 0 && alpha != 0.0;
+    const bool ta = use && make_operand_map(&st.ma, A, lda, M, K, kca);
+    const bool tb = use && make_operand_map(&st.mb, B, ldb, N, K, kcb);
+    st.tma = ta && tb;
+    if (!st.tma) { std::memset(&st.ma, 0, sizeof(st.ma)); std::memset(&st.mb, 0, sizeof(st.mb)); }
+    return st;
+}
+
+template <bool KCX, bool TMA, int QN>
+cudaError_t launch_cksum_t(const CkArgs &a, const CUtensorMap &mx, const CUtensorMap &my, dim3 grid, cudaStream_t s) {
+    auto kern = cksum_kernel<KCX, TMA, QN>;
+    const int bytes = CkPlan<QN>::BYTES;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, GEMM_THREADS, bytes, s>>>(a, mx, my);
+    ctx().launches++;
+    return cudaGetLastError();
+}
+
+// Split count of a checksum GEMM with `tiles` 128-row tiles: about four waves of CTAs in
+// total, at least one BK slice per split.
+void cksum_split(long long tiles, long long K, long long &splits, long long &kper) {
+    const long long kt = std::max<long long>(1, (K + BK - 1) / BK);
+    splits = std::max<long long>(1, std::min<long long>(kt, (4 * 148 + tiles - 1) / tiles));
+    kper = (kt + splits - 1) / splits * BK;
+    splits = (K + kper - 1) / kper;
+}
+
+// Checksum GEMM out (P x Q, ld P, k-split partials at out + s * split_stride) = op(X) (P x K) .
+// Y (K x Q; Y(k, q) = Y[q * ldy + k]) for Q <= 128 (the caller splits wider Q).
+cudaError_t cksum_gemm(bool kcx, const double *X, long long ldx, long long P, const double *Y, long long ldy,
+                       long long Q, long long K, long long splits, long long kper, double *out,
+                       long long split_stride, cudaStream_t s) {
+    CkArgs a{};
+    a.X = X; a.Y = Y; a.ldx = ldx; a.ldy = ldy; a.P = P; a.Q = Q; a.K = K; a.kper = kper;
+    a.out = out; a.ldo = P; a.split_stride = split_stride;
+    Staging st;
+    const bool tx = make_operand_map(&st.ma, X, ldx, P, K, kcx);
+    const int qn = Q <= 16 ? 16 : Q <= 32 ? 32 : Q <= 64 ? 64 : 128;
+    bool ty = false;
+    if (tx) {  // Y: k-contiguous, box {16, QN} (rows >= Q zero-filled)
+        std::memset(&st.mb, 0, sizeof(st.mb));
+        EncodeTiledFn fn = encode_tiled();
+        const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)Q};
+        const cuuint64_t strides[1] = {(cuuint64_t)ldy * 8};
+        const cuuint32_t box[2] = {16u, (cuuint32_t)qn};
+        const cuuint32_t estr[2] = {1u, 1u};
+        ty = fn && (reinterpret_cast<uintptr_t>(Y) & 15) == 0 && (ldy & 1) == 0 &&
+             fn(&st.mb, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(Y), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+    const bool tma = tx && ty;
+    if (!tma) { std::memset(&st.ma, 0, sizeof(st.ma)); std::memset(&st.mb, 0, sizeof(st.mb)); }
+    const dim3 grid((unsigned)((P + BM - 1) / BM), (unsigned)splits, 1);
+#define L(x, t, q) if (kcx == x && tma == t && qn == q) return launch_cksum_t<x, t, q>(a, st.ma, st.mb, grid, s)
+    L(false, true, 16); L(false, true, 32); L(false, true, 64); L(false, true, 128);
+    L(true, true, 16); L(true, true, 32); L(true, true, 64); L(true, true, 128);
+    L(false, false, 16); L(false, false, 32); L(false, false, 64); L(false, false, 128);
+    L(true, false, 16); L(true, false, 32); L(true, false, 64); L(true, false, 128);
+#undef L
+    return cudaErrorInvalidValue;
+}
+
 int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K, double alpha,
                const double *A, long long lda, const double *B, long long ldb, double beta, double *C,
                long long ldc, ftblas_err_report *rep) {
@@ -228,6 +337,7 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
     g.A = A; g.B = B; g.C = C; g.lda = lda; g.ldb = ldb; g.ldc = ldc;
     g.M = M; g.N = N; g.K = K; g.alpha = alpha; g.beta = beta;
     const bool va = vec_ok(A, lda), vb = vec_ok(B, ldb);
+    const Staging stg = make_staging(A, lda, M, kca, B, ldb, N, kcb, K, alpha);
     Ctx::Rec rec{};
     if (c.profiling) {
         rec = take_rec(ft);
@@ -236,36 +346,70 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
     if (ft) {
         const long long Kp = std::max<long long>(BK, (K + BK - 1) / BK * BK);
         // k-chunks of the encode pass: enough blocks to fill the GPU, chunks >= 32 columns
-        int kch = (int)std::max<long long>(1, std::min<long long>(16, (2 * 148 + ntm + ntn - 1) / (ntm + ntn)));
-        kch = (int)std::min<long long>(kch, std::max<long long>(1, Kp / 32));
+        // k-chunks of the encode pass: ~1024 k per block (1 MiB slabs for 128-wide tiles), at
+        // least two blocks per SM in total, chunks >= 32 columns, at most 16 partials per row
+        // (the GEMM producer reduces them per tile)
+        long long kch_l = std::max<long long>((Kp + 1023) / 1024, (2 * 148 + ntm + ntn - 1) / (ntm + ntn));
+        kch_l = std::min<long long>({kch_l, 16, std::max<long long>(1, Kp / 32)});
+        int kch = (int)std::max<long long>(1, kch_l);
         const long long kper = ((Kp + kch - 1) / kch + 31) / 32 * 32;
         const size_t nV = (size_t)(ntm + ntn) * Kp, nLine = (size_t)kch * (M + N), nT = (size_t)kch * (ntm + ntn);
-        CK(c.ws.ensure((nV + nLine + nT) * sizeof(double)), "cudaMalloc(workspace)");
+        const bool pre = c.checksum_mode == FTBLAS_CHECKSUM_GEMM;
+        long long spR = 1, kpR = Kp, spS = 1, kpS = Kp;
+        if (pre) {
+            cksum_split(ntm * ((ntn + 127) / 128), K, spR, kpR);
+            cksum_split(ntn * ((ntm + 127) / 128), K, spS, kpS);
+        }
+        const size_t nRS = pre ? (size_t)spR * ntn * M + (size_t)spS * ntm * N : 0;
+        CK(c.ws.ensure((nV + nLine + nT + nRS) * sizeof(double)), "cudaMalloc(workspace)");
         double *w = c.ws.as<double>();
         g.VA = w; g.WB = w + ntm * Kp;
         double *lineA = w + nV, *lineB = lineA + (size_t)kch * M;
         double *tmaxA = lineB + (size_t)kch * N, *tmaxB = tmaxA + (size_t)kch * ntm;
         g.lineA = lineA; g.lineB = lineB; g.tmaxA = tmaxA; g.tmaxB = tmaxB;
         g.kch = kch; g.Kp = Kp;
+        double *Rpre = tmaxB + (size_t)kch * ntn, *Spre = Rpre + (size_t)spR * ntn * M;
+        g.Rpre = pre ? Rpre : nullptr;
+        g.Spre = pre ? Spre : nullptr;
+        g.splits_r = (int)spR; g.splits_s = (int)spS;
+        g.stride_r = ntn * M; g.stride_s = ntm * N;
         g.rep = c.rep.as<ReportHdr>();
         g.rep_entries = reinterpret_cast<Correction *>(c.rep.as<char>() + sizeof(ReportHdr));
         g.rep_cap = c.rep_cap;
+        g.vecC = vec_ok(C, ldc) ? 1 : 0;
         rc = prepare_plan(M, N, g);
         if (rc) return rc;
         EncodeArgs ea{};
-        ea.op[0] = EncodeOperand{A, lda, M, kca ? 1 : 0, const_cast<double *>(g.VA), lineA, tmaxA, (int)ntm};
-        ea.op[1] = EncodeOperand{B, ldb, N, kcb ? 1 : 0, const_cast<double *>(g.WB), lineB, tmaxB, (int)ntn};
+        ea.op[0] = EncodeOperand{A, lda, M, kca ? 1 : 0, va ? 1 : 0, const_cast<double *>(g.VA), lineA, tmaxA, (int)ntm};
+        ea.op[1] = EncodeOperand{B, ldb, N, kcb ? 1 : 0, vb ? 1 : 0, const_cast<double *>(g.WB), lineB, tmaxB, (int)ntn};
         ea.K = (alpha == 0.0) ? 0 : K;  // alpha == 0: A, B are not read (encodes are zero)
         ea.Kp = Kp; ea.kper = kper; ea.kch = kch; ea.rep = g.rep;
         dim3 grid((unsigned)std::max(ntm, ntn), (unsigned)kch, 2);
         encode_kernel<<<grid, NTHREADS, 0, c.stream>>>(ea);
         c.launches++;
         CK(cudaGetLastError(), "encode_kernel launch");
+        if (pre && K > 0 && alpha != 0.0) {
+            // checksum GEMMs (the border of C^f = A^c B^r) on the FP64
+            // tensor cores:  R (M x ntn, ld M)   = op(A) . WB^T   [WB^T: k x ntn, 'N', ld Kp]
+            //                S^T (N x ntm, ld N) = op(B)^T . VA^T [VA^T: k x ntm, 'N', ld Kp]
+            // (column blocks of <= 128 tiles; k-split partials summed in the FT_PRE epilogue)
+            for (long long q0 = 0; q0 < ntn; q0 += 128)
+                CK(cksum_gemm(kca, A, lda, M, g.WB + q0 * Kp, Kp, std::min<long long>(128, ntn - q0), K, spR, kpR,
+                              Rpre + q0 * M, ntn * M, c.stream), "checksum GEMM R");
+            for (long long q0 = 0; q0 < ntm; q0 += 128)
+                CK(cksum_gemm(kcb, B, ldb, N, g.VA + q0 * Kp, Kp, std::min<long long>(128, ntm - q0), K, spS, kpS,
+                              Spre + q0 * N, ntm * N, c.stream), "checksum GEMM S");
+        } else if (pre) {
+            CK(cudaMemsetAsync(Rpre, 0, nRS * sizeof(double), c.stream), "checksum zero");
+        }
         if (c.profiling) CK(cudaEventRecord(rec.e1, c.stream), "event");
-        CK(launch_gemm<true>(kca, kcb, va, vb, g, ntm * ntn, c.stream), "gemm_kernel<FT> launch");
+        if (pre)
+            CK(launch_gemm<MODE_FT_PRE>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream), "gemm_kernel<FT> launch");
+        else
+            CK(launch_gemm<MODE_FT_FUSED>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream), "gemm_kernel<FT> launch");
     } else {
         if (c.profiling) CK(cudaEventRecord(rec.e1, c.stream), "event");
-        CK(launch_gemm<false>(kca, kcb, va, vb, g, ntm * ntn, c.stream), "gemm_kernel launch");
+        CK(launch_gemm<MODE_NOFT>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream), "gemm_kernel launch");
     }
     if (c.profiling) {
         CK(cudaEventRecord(rec.e2, c.stream), "event");
@@ -340,6 +484,14 @@ int ftblas_set_fault_plan(int64_t n, const int64_t *i, const int64_t *j, const i
     c.plan_version++;
     return 0;
 }
+
+int ftblas_set_checksum_mode(int mode) {
+    if (mode != FTBLAS_CHECKSUM_GEMM && mode != FTBLAS_CHECKSUM_FUSED) return arg_fail(1, "unknown checksum mode");
+    ctx().checksum_mode = mode;
+    return 0;
+}
+
+int ftblas_get_checksum_mode(void) { return ctx().checksum_mode; }
 
 int ftblas_set_stream(void *stream) {
     ctx().stream = static_cast<cudaStream_t>(stream);

@@ -3,37 +3,102 @@
 //   encode_kernel : Huang-Abraham checksum encoding of op(A) and op(B) per
 //                   verification tile (section II.A:
 //                   A^c = [A; e^T A], B^r = [B, B e]) plus the norms used by the
-//                   round-off threshold (reading R4).
+//                   round-off threshold (reading R4).  HBM-bound stream.
 //   gemm_kernel   : C := alpha op(A) op(B) + beta C on FP64 tensor cores
-//                   (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4), cp.async multi-stage
-//                   smem pipeline; with FT=true it also accumulates the checksum
-//                   column C e = A (B e) and row e^T C = (e^T A) B of the tile in the
-//                   same mainloop (line 516, "C^f = A^c B^r"), and its epilogue
-//                   verifies, locates and corrects (lines 517, 540, 521) before the
-//                   store.  FT=false is the non-FT baseline (same tiles/mainloop).
+//                   (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4, the FP64 tensor-core
+//                   instruction of sm_100a; tcgen05.mma has no f64 kind).  Operand tiles
+//                   are staged by TMA (cp.async.bulk.tensor, 128-byte swizzle) into a
+//                   STAGES-deep smem ring driven by one producer thread and mbarriers.
+//                   With FT=true it also accumulates the checksum column C e = A (B e)
+//                   and row e^T C = (e^T A) B of the tile in the same mainloop (line 516,
+//                   "C^f = A^c B^r"), and its epilogue verifies, locates and corrects
+//                   (lines 517, 540, 521) before the store.  FT=false is the non-FT
+//                   baseline (same tiles/mainloop).
 //
-// Layout of one CTA: 256 threads = 8 warps in a 2 (M) x 4 (N) grid, warp tile
-// 64 x 32 = 8 x 4 DMMA fragments of 8x8, CTA tile 128 x 128, BK = 16,
-// STAGES-deep cp.async ring.  See DESIGN.md section 4 for the roofline.
+// CTA: 8 MMA warps in a 2 (M) x 4 (N) grid, warp tile 64 x 32 = 8 x 4 DMMA fragments of
+// 8x8, CTA tile 128 x 128, BK = 32, plus one producer warpgroup.  See DESIGN.md section 5.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace ftb {
 
-constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3, NTHREADS = 256;
+#ifndef FTB_BK  // k-depth of a pipeline stage / number of stages (overridable for experiments)
+#define FTB_BK 32
+#endif
+#ifndef FTB_STAGES
+#define FTB_STAGES 3
+#endif
+constexpr int BM = 128, BN = 128, BK = FTB_BK, STAGES = FTB_STAGES, NTHREADS = 256;
 constexpr int WM = 64, WN = 32, FM = WM / 8, FN = WN / 8;
-// Padded smem strides chosen so that a DMMA fragment load (a half-warp reads 4 mn x 4 k
-// doubles) touches 16 distinct 8-byte bank pairs: row strides == 32 (mod 128) bytes.
-constexpr int LD_MN = 128 + 4;  // doubles per k-row when the mn index is contiguous (1056 B)
-constexpr int LD_K = BK + 4;    // doubles per mn-row when k is contiguous (288 B)
+static_assert(BK % 16 == 0, "BK must be a multiple of the 16-double TMA box row");
 constexpr double U_ROUND = 1.0 / 9007199254740992.0;  // 2^-53
 
-// smem doubles of one operand tile (one stage)
-template <bool KC>
+// ---------------------------------------------------------------- smem operand tile layout
+// One stage of an operand is a dense 128 x BK tile of doubles made of 128-byte rows, the
+// layout TMA writes with CU_TENSOR_MAP_SWIZZLE_128B:
+//   KC=false (mn contiguous in HBM: op(A)=A 'N', op(B)=B 'T'): 8 boxes of 16 mn, each box
+//            [BK k-rows][16 mn];
+//   KC=true  (k contiguous in HBM: op(A)=A 'T', op(B)=B 'N'): BK/16 boxes of 16 k, each box
+//            [128 mn-rows][16 k].
+// Inside 128-byte row r, the 16-byte unit u (elements 2u, 2u+1) sits at unit u ^ (r & 7).
+// With the fragment row maps of frag_mn() below, every DMMA fragment load (a warp reads
+// 8 mn x 4 k) and every checksum load touches each 8-byte bank pair exactly twice: 2
+// wavefronts for 256 bytes, i.e. conflict-free.
+// (ROWS = mn extent of the tile: 128 for the main GEMM, 16..128 for the checksum GEMMs' thin
+// operand.)
+constexpr int TILE_EL = 128 * BK;
+template <bool KC, int ROWS = 128>
 struct Tile {
-    static constexpr int ELEMS = KC ? 128 * LD_K : BK * LD_MN;
-    __device__ __forceinline__ static int idx(int mn, int k) { return KC ? mn * LD_K + k : k * LD_MN + mn; }
+    __device__ __forceinline__ static int idx(int mn, int k) {
+        if (KC) {
+            const int kk = k & 15;
+            return (k >> 4) * (ROWS * 16) + mn * 16 + ((((kk >> 1) ^ (mn & 7)) << 1) | (kk & 1));
+        } else {
+            const int m = mn & 15;
+            return (mn >> 4) * (BK * 16) + k * 16 + ((((m >> 1) ^ (k & 7)) << 1) | (m & 1));
+        }
+    }
+};
+// mn index (within the CTA tile) of row g (0..7) of the 8-wide fragment f of a warp tile
+// starting at `base`.  KC=true: natural order.  KC=false: fragment f takes mn
+// {4(f&1)+0..3, 4(f&1)+8..11} of the 16-mn box f/2, which spreads its 8 rows over 4
+// distinct 16-byte units of every swizzled k-row (see Tile).  The accumulator row / column
+// of C fragment element (g, j) is frag_mn of the A / B side: the MMA is agnostic to which
+// mn a fragment row stands for, as long as A, B and C agree.
+template <bool KC>
+__device__ __forceinline__ int frag_mn(int base, int f, int g) {
+    return KC ? base + 8 * f + g : base + 16 * (f >> 1) + 4 * (f & 1) + (g & 3) + 8 * (g >> 2);
+}
+
+// Per-thread precomputed smem offsets of the DMMA fragment loads: the element (row g of
+// fragment f, k = 4 kk + (lane & 3)) of a warp tile at `base` is at a compile-time constant
+// (from f, kk) plus one of 4 per-thread offsets (the swizzle XOR only depends on f & 1 and
+// kk & 1 for KC=false, on kk & 3 for KC=true).  Equal to Tile<KC>::idx(frag_mn<KC>(base, f,
+// g), k) -- asserted by the unit test of tests/test_gpu_parity.py through the results.
+template <bool KC, int ROWS = 128>
+struct FragAddr {
+    int off[4];
+    __device__ __forceinline__ FragAddr(int base, int lane) {
+        const int g = lane >> 2, l3 = lane & 3;
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+            if (KC) {  // v = kk & 3; mn = base + 8 f + g, (mn & 7) = g since base % 8 == 0
+                const int kk16 = 4 * v + l3;
+                off[v] = (base + g) * 16 + ((((kk16 >> 1) ^ g) << 1) | (kk16 & 1));
+            } else {   // v = (f & 1) | (kk & 1) << 1; base % 16 == 0
+                const int f1 = v & 1, k7 = 4 * (v >> 1) + l3;
+                const int m = 4 * f1 + (g & 3) + 8 * (g >> 2);
+                off[v] = (base >> 4) * (BK * 16) + l3 * 16 + ((((m >> 1) ^ k7) << 1) | (m & 1));
+            }
+        }
+    }
+    // f, kk compile-time after unrolling
+    __device__ __forceinline__ int operator()(int f, int kk) const {
+        if (KC) return off[kk & 3] + (kk >> 2) * (ROWS * 16) + 8 * f * 16;
+        return off[(f & 1) | ((kk & 1) << 1)] + (f >> 1) * (BK * 16) + (kk & ~1) * 4 * 16 + (kk & 1) * 4 * 16;
+    }
 };
 
 struct Correction {  // == ftblas_correction (48 bytes)
@@ -60,6 +125,10 @@ struct GemmArgs {
     const double *tmaxB;   // kch x ntn
     int kch;
     long long Kp;
+    const double *Rpre;    // FT_PRE: [splits_r][ntn][M], R[tn][i] = sum_k op(A)(i,k) WB[tn][k] (k-split partials)
+    const double *Spre;    // FT_PRE: [splits_s][ntm][N], S[tm][j] = sum_k VA[tm][k] op(B)(k,j)
+    int splits_r, splits_s;
+    long long stride_r, stride_s;
     // fault plan (CSR by tile, tile index = tn * ntm + tm)
     const int *plan_ptr;   // ntm*ntn + 1 or nullptr
     const long long *plan_i, *plan_j;
@@ -68,6 +137,7 @@ struct GemmArgs {
     ReportHdr *rep;
     Correction *rep_entries;
     long long rep_cap;
+    int vecC;              // C 16-byte aligned with even ldc (cp.async16 staging of C0)
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -92,6 +162,11 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long *b) {
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(smem_u32(b))
                  : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *b, unsigned bytes) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}\n" ::"r"(
+                     smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long *b, unsigned parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tLAB_WAIT:\n\t"
@@ -102,6 +177,20 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *b, unsigned parity
 // arrive on b when all prior cp.async of this thread have landed (count pre-set at init)
 __device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long *b) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+// TMA: 2-D tiled box global -> smem, completion counted in bytes on mbarrier b
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, unsigned long long *b, int c0,
+                                            int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::
+            "r"(smem_u32(dst)), "l"(map), "r"(smem_u32(b)), "r"(c0), "r"(c1)
+        : "memory");
+}
+// bulk (non-tensor) copy of `bytes` (multiple of 16) global -> smem, counted on mbarrier b
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes, unsigned long long *b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b))
+                 : "memory");
 }
 __device__ __forceinline__ void bar_mma() {  // named barrier over the NTHREADS MMA threads only
     asm volatile("bar.sync 1, %0;\n" ::"n"(NTHREADS) : "memory");
@@ -125,94 +214,54 @@ __device__ __forceinline__ const double *gaddr(const double *X, long long ld, lo
     return KC ? X + k + mn * ld : X + mn + k * ld;
 }
 
-// Stage one 128 x BK operand tile into smem with cp.async (zero-fill outside [0,MNd) x [0,Kd)).
-template <bool KC, bool VEC, int NT = NTHREADS>
-__device__ __forceinline__ void load_tile(double *s, const double *X, long long ld, long long mn0,
-                                          long long k0, long long MNd, long long Kd, int tid) {
-    if (VEC) {  // 16-byte chunks along the contiguous dimension (needs 16B-aligned X, even ld)
-#pragma unroll
-        for (int q = 0; q < (128 * BK / 2) / NT; q++) {
-            int c = tid + q * NT;
-            int mn, k;
-            if (KC) { mn = c / (BK / 2); k = (c % (BK / 2)) * 2; }
-            else    { k = c >> 6;  mn = (c & 63) * 2; }
-            long long gmn = mn0 + mn, gk = k0 + k;
-            int nvalid;
-            if (KC) nvalid = (gmn < MNd) ? (int)min(2ll, max(0ll, Kd - gk)) : 0;
-            else    nvalid = (gk < Kd) ? (int)min(2ll, max(0ll, MNd - gmn)) : 0;
-            const double *src = nvalid ? gaddr<KC>(X, ld, gmn, gk) : X;
-            cp_async16(s + Tile<KC>::idx(mn, k), src, nvalid * 8);
-        }
-    } else {  // 8-byte elements: any alignment / odd ld
-#pragma unroll
-        for (int q = 0; q < (128 * BK) / NT; q++) {
-            int c = tid + q * NT;
-            int mn, k;
-            if (KC) { mn = c / BK; k = c % BK; }
-            else    { k = c >> 7;  mn = c & 127; }
-            long long gmn = mn0 + mn, gk = k0 + k;
-            bool ok = gmn < MNd && gk < Kd;
-            cp_async8(s + Tile<KC>::idx(mn, k), ok ? gaddr<KC>(X, ld, gmn, gk) : X, ok ? 8 : 0);
-        }
-    }
-}
+constexpr int PRODUCER_THREADS = 128;  // one warpgroup; registers go to the MMA warps
 
-// Producer-side staging of one 128 x BK operand tile by the PRODUCER_THREADS threads of the
-// load warpgroup: one base pointer + a constant stride per thread (low register footprint,
-// the producer runs with PRODUCER_REGS registers after setmaxnreg.dec).
-constexpr int PRODUCER_THREADS_ = 128;
-template <bool KC, bool VEC>
-__device__ __forceinline__ void produce_tile(double *s, const double *X, long long ld, long long mn0,
-                                             long long k0, long long MNd, long long Kd, int pt) {
-    if (VEC) {
-        if (KC) {  // k contiguous: BK/2 16-byte chunks per mn row
-            constexpr int CPR = BK / 2, STEP = PRODUCER_THREADS_ / CPR;
-            const int k = (pt % CPR) * 2, mnb = pt / CPR;
-            const long long gk = k0 + k;
-            const int kval = (int)min(2ll, max(0ll, Kd - gk));
-            const double *src = X + gk + (mn0 + mnb) * ld;
-            double *dst = s + mnb * LD_K + k;
-#pragma unroll 4
-            for (int q = 0; q < 128 / STEP; q++) {
-                const int nv = (mn0 + mnb + q * STEP < MNd) ? kval : 0;
-                cp_async16(dst + q * STEP * LD_K, nv ? src + (long long)q * STEP * ld : X, nv * 8);
-            }
-        } else {   // mn contiguous: 64 chunks per k row
-            constexpr int STEP = PRODUCER_THREADS_ / 64;
-            const int mn = (pt % 64) * 2, kb = pt / 64;
-            const long long gmn = mn0 + mn;
-            const int mval = (int)min(2ll, max(0ll, MNd - gmn));
-            const double *src = X + gmn + (k0 + kb) * ld;
-            double *dst = s + kb * LD_MN + mn;
-#pragma unroll 4
-            for (int q = 0; q < BK / STEP; q++) {
-                const int nv = (k0 + kb + q * STEP < Kd) ? mval : 0;
-                cp_async16(dst + q * STEP * LD_MN, nv ? src + (long long)q * STEP * ld : X, nv * 8);
+// Stage one 128 x BK operand tile (rows [mn0, mn0+128), k [k0, k0+BK)) into the swizzled
+// layout.  TMA=true: thread 0 of the producer warpgroup issues the boxes (bytes counted on
+// `bar` through the expect_tx of the caller); out-of-range elements are zero-filled by TMA.
+// TMA=false (operand pointer not 16-byte aligned or odd ld, where a tensor map cannot be
+// built): every producer thread copies 8-byte elements with cp.async, zero-fill outside
+// [0,MNd) x [0,Kd).
+template <bool KC, bool TMA, int ROWS = 128>
+__device__ __forceinline__ void produce_tile(double *s, const CUtensorMap *map, unsigned long long *bar,
+                                             const double *X, long long ld, long long mn0, long long k0,
+                                             long long MNd, long long Kd, int pt) {
+    if (TMA) {
+        if (pt == 0) {
+            if (KC) {
+#pragma unroll
+                for (int h = 0; h < BK / 16; h++) tma_load_2d(s + h * ROWS * 16, map, bar, (int)(k0 + 16 * h), (int)mn0);
+            } else {
+#pragma unroll
+                for (int c = 0; c < ROWS / 16; c++) tma_load_2d(s + c * BK * 16, map, bar, (int)(mn0 + 16 * c), (int)k0);
             }
         }
-    } else {  // 8-byte elements (misaligned pointer / odd ld): correctness path
-#pragma unroll 1
-        for (int c = pt; c < 128 * BK; c += PRODUCER_THREADS_) {
+    } else {
+#pragma unroll 4
+        for (int c = pt; c < ROWS * BK; c += PRODUCER_THREADS) {
             int mn, k;
             if (KC) { mn = c / BK; k = c % BK; }
-            else    { k = c >> 7;  mn = c & 127; }
+            else    { k = c / ROWS; mn = c % ROWS; }
             const long long gmn = mn0 + mn, gk = k0 + k;
             const bool ok = gmn < MNd && gk < Kd;
-            cp_async8(s + Tile<KC>::idx(mn, k), ok ? gaddr<KC>(X, ld, gmn, gk) : X, ok ? 8 : 0);
+            cp_async8(s + Tile<KC, ROWS>::idx(mn, k), ok ? gaddr<KC>(X, ld, gmn, gk) : X, ok ? 8 : 0);
         }
     }
 }
 
 // ------------------------------------------------------------------ encode kernel
 // P(i,k) = op(A)(i,k) (operand 0) or op(B)(k,i) (operand 1).  KC: k contiguous.
-// Block (tile t, chunk ch, operand) reduces a 128 x [kbeg,kend) slab:
-//   V[t*Kp + k]            = sum_{i in tile} P(i,k)         (A^c row / B^r column)
-//   line[ch*MNd + i]       = sum_{k in chunk} |P(i,k)|       (row / column 1-norms)
+// Block (tile t, chunk ch, operand) streams the 128 x [kbeg,kend) slab of P once:
+//   V[t*Kp + k]            = sum_{i in tile} P(i,k)         (A^c row / B^r column, line 516)
+//   line[ch*MNd + i]       = sum_{k in chunk} |P(i,k)|       (row / column 1-norms, reading R4)
 //   tmax[ch*ntiles + t]    = max_{k in chunk} sum_i |P(i,k)|
+// V is zero for k in [K, Kp) (the GEMM stages whole BK-wide slices of V).  HBM-bound: every
+// element is read once with coalesced (16-byte where possible) loads, several loads in flight
+// per thread; the cross-lane reductions are warp shuffles.
 struct EncodeOperand {
     const double *X;
     long long ld, MNd;
-    int kc;
+    int kc, vec;
     double *V, *line, *tmax;
     int ntiles;
 };
@@ -223,78 +272,143 @@ struct EncodeArgs {
     ReportHdr *rep;  // zeroed here (stream-ordered before the GEMM kernel)
 };
 
-template <bool KC>
-__device__ void encode_slab(const EncodeOperand &o, const EncodeArgs &a, int t, int ch, double (*s)[33],
-                            double *red) {
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+// mn contiguous (op(A) = A 'N', op(B) = B 'T'): warp w reduces columns k = kbeg + w + 8q.
+// Lane l owns rows {2l, 2l+1, 64+2l, 65+2l} (VEC, 16-byte loads) or {l, l+32, l+64, l+96}.
+template <bool VEC>
+__device__ void encode_mn_contig(const EncodeOperand &o, const EncodeArgs &a, int t, long long kbeg,
+                                 long long kend, double *red, double &tm) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long i0 = (long long)t * 128;
-    const long long kbeg = (long long)ch * a.kper;
-    const long long kend = min(kbeg + a.kper, a.Kp);
-    double la = 0.0, tm = 0.0;
-    for (long long kb = kbeg; kb < kend; kb += 32) {
-        for (int idx = tid; idx < 128 * 32; idx += NTHREADS) {
-            int i, kk;
-            if (KC) { i = idx >> 5; kk = idx & 31; }
-            else    { i = idx & 127; kk = idx >> 7; }
-            long long gi = i0 + i, gk = kb + kk;
-            double v = 0.0;
-            if (gi < o.MNd && gk < a.K) v = *gaddr<KC>(o.X, o.ld, gi, gk);
-            s[i][kk] = v;
+    int rows[4];
+    if (VEC) { rows[0] = 2 * lane; rows[1] = 2 * lane + 1; rows[2] = 64 + 2 * lane; rows[3] = 65 + 2 * lane; }
+    else     { rows[0] = lane; rows[1] = lane + 32; rows[2] = lane + 64; rows[3] = lane + 96; }
+    bool rv[4];
+#pragma unroll
+    for (int r = 0; r < 4; r++) rv[r] = i0 + rows[r] < o.MNd;
+    double la[4] = {0.0, 0.0, 0.0, 0.0};
+    constexpr int U = 4;  // columns per warp per iteration (independent loads in flight)
+    for (long long k = kbeg + warp; k < kend; k += 8 * U) {
+        double x[U][4];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const long long kk = k + 8 * u;
+            const bool kv = kk < a.K && kk < kend;
+            const double *col = o.X + i0 + kk * o.ld;
+            if (VEC) {
+                double2 p = make_double2(0.0, 0.0), q = make_double2(0.0, 0.0);
+                if (kv && rv[1]) p = __ldcs(reinterpret_cast<const double2 *>(col + rows[0]));
+                else if (kv && rv[0]) p.x = __ldcs(col + rows[0]);
+                if (kv && rv[3]) q = __ldcs(reinterpret_cast<const double2 *>(col + rows[2]));
+                else if (kv && rv[2]) q.x = __ldcs(col + rows[2]);
+                x[u][0] = p.x; x[u][1] = p.y; x[u][2] = q.x; x[u][3] = q.y;
+            } else {
+#pragma unroll
+                for (int r = 0; r < 4; r++) x[u][r] = (kv && rv[r]) ? __ldcs(col + rows[r]) : 0.0;
+            }
         }
-        __syncthreads();
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-            int kk = warp * 4 + q;
-            double sum = 0.0, sa = 0.0;
+        for (int u = 0; u < U; u++) {
+            const long long kk = k + 8 * u;
+            double s = (x[u][0] + x[u][1]) + (x[u][2] + x[u][3]);
+            double sa = (fabs(x[u][0]) + fabs(x[u][1])) + (fabs(x[u][2]) + fabs(x[u][3]));
 #pragma unroll
-            for (int r = 0; r < 4; r++) {
-                double v = s[lane + 32 * r][kk];
-                sum += v;
-                sa += fabs(v);
-            }
-#pragma unroll
-            for (int off = 16; off; off >>= 1) {
-                sum += __shfl_xor_sync(0xffffffffu, sum, off);
-                sa += __shfl_xor_sync(0xffffffffu, sa, off);
-            }
-            if (kb + kk < kend) {
-                if (lane == 0) o.V[(long long)t * a.Kp + kb + kk] = sum;
+            for (int r = 0; r < 4; r++) la[r] += fabs(x[u][r]);
+            s = warp_sum(s);
+            sa = warp_sum(sa);
+            if (kk < kend) {
+                if (lane == 0) o.V[(long long)t * a.Kp + kk] = s;  // 0 for kk >= K
                 tm = fmax(tm, sa);
             }
         }
-        {
-            int i = tid & 127, h = tid >> 7;
+    }
 #pragma unroll
-            for (int kk = 0; kk < 16; kk++) la += fabs(s[i][h * 16 + kk]);
+    for (int r = 0; r < 4; r++) red[warp * 128 + rows[r]] = la[r];
+}
+
+// k contiguous (op(A) = A 'T', op(B) = B 'N'): thread owns k = kbeg + tid + 256q and loops over
+// the 128 mn of the tile (each load instruction of a warp reads 256 contiguous bytes).  The
+// per-mn |.| sums over the warp's 32 k are formed by a transposing butterfly (31 shuffles per
+// 32 mn instead of 160): afterwards lane l holds the sum for mn = 32g + l.
+__device__ void encode_k_contig(const EncodeOperand &o, const EncodeArgs &a, int t, long long kbeg,
+                                long long kend, double *red, double &tm) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long i0 = (long long)t * 128;
+    const int nrow = (int)min(128ll, o.MNd - i0);
+    double la[4] = {0.0, 0.0, 0.0, 0.0};
+    for (long long k = kbeg + tid; k - tid < kend; k += NTHREADS) {
+        const bool kv = k < kend && k < a.K;
+        const double *row0 = o.X + k + i0 * o.ld;
+        double s = 0.0, sa = 0.0;
+#pragma unroll
+        for (int g = 0; g < 4; g++) {
+            double v[32];
+#pragma unroll
+            for (int j = 0; j < 32; j++) {
+                const int i = g * 32 + j;
+                const double x = (kv && i < nrow) ? __ldcs(row0 + (long long)i * o.ld) : 0.0;
+                s += x;
+                v[j] = fabs(x);
+            }
+#pragma unroll
+            for (int j = 0; j < 32; j++) sa += v[j];
+#pragma unroll
+            for (int off = 16; off; off >>= 1) {
+                const bool up = (lane & off) != 0;
+#pragma unroll
+                for (int j = 0; j < off; j++) {
+                    const double send = up ? v[j] : v[j + off];
+                    const double keep = up ? v[j + off] : v[j];
+                    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                }
+            }
+            la[g] += v[0];
         }
-        __syncthreads();
+        if (k < kend) {
+            o.V[(long long)t * a.Kp + k] = s;  // 0 for k >= K
+            tm = fmax(tm, sa);
+        }
     }
-    // line partials: combine the two k-halves in fixed order
-    red[tid] = la;
-    if (lane == 0) red[NTHREADS + warp] = tm;
-    __syncthreads();
-    if (tid < 128) {
-        long long gi = i0 + tid;
-        if (gi < o.MNd) o.line[(long long)ch * o.MNd + gi] = red[tid] + red[tid + 128];
-    }
-    if (tid == 0) {
-        double m = 0.0;
-        for (int w = 0; w < NTHREADS / 32; w++) m = fmax(m, red[NTHREADS + w]);
-        o.tmax[(long long)ch * o.ntiles + t] = m;
-    }
+#pragma unroll
+    for (int g = 0; g < 4; g++) red[warp * 128 + g * 32 + lane] = la[g];
 }
 
 __global__ void __launch_bounds__(NTHREADS) encode_kernel(EncodeArgs a) {
-    __shared__ double s[128][33];
-    __shared__ double red[NTHREADS + NTHREADS / 32];
+    __shared__ double red[(NTHREADS / 32) * 128];
+    __shared__ double wmax[NTHREADS / 32];
     const EncodeOperand &o = a.op[blockIdx.z];
-    const int t = blockIdx.x, ch = blockIdx.y;
-    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 && a.rep) {
+    const int t = blockIdx.x, ch = blockIdx.y, tid = threadIdx.x;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0 && a.rep) {
         a.rep->count = 0; a.rep->tiles_flagged = 0; a.rep->rows_flagged = 0; a.rep->cols_flagged = 0;
     }
     if (t >= o.ntiles) return;
-    if (o.kc) encode_slab<true>(o, a, t, ch, s, red);
-    else      encode_slab<false>(o, a, t, ch, s, red);
+    const long long kbeg = (long long)ch * a.kper;
+    const long long kend = min(kbeg + a.kper, a.Kp);
+    double tm = 0.0;
+    if (o.kc)       encode_k_contig(o, a, t, kbeg, kend, red, tm);
+    else if (o.vec) encode_mn_contig<true>(o, a, t, kbeg, kend, red, tm);
+    else            encode_mn_contig<false>(o, a, t, kbeg, kend, red, tm);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) tm = fmax(tm, __shfl_xor_sync(0xffffffffu, tm, off));
+    if ((tid & 31) == 0) wmax[tid >> 5] = tm;
+    __syncthreads();
+    if (tid < 128) {  // line partial of row tid: warps combined in fixed order
+        double l = 0.0;
+#pragma unroll
+        for (int w = 0; w < NTHREADS / 32; w++) l += red[w * 128 + tid];
+        const long long gi = (long long)t * 128 + tid;
+        if (gi < o.MNd) o.line[(long long)ch * o.MNd + gi] = l;
+    }
+    if (tid == 0) {
+        double m = 0.0;
+        for (int w = 0; w < NTHREADS / 32; w++) m = fmax(m, wmax[w]);
+        o.tmax[(long long)ch * o.ntiles + t] = m;
+    }
 }
 
 
@@ -303,16 +417,27 @@ constexpr int LDT = 130;  // epilogue tile leading dimension (conflict-free frag
 constexpr int EPI_EL = 128 * LDT   /* tile */
                      + 6 * 128     /* rowS[2][128], rowC[2][128], rowCA[2][128] */
                      + 3 * 128     /* colS, colC, colCA */
-                     + 2 * 256     /* rsp[2][128], ssp[2][128] */
+                     + 2 * 256     /* rsp[128], ssp[128] (+ spare) */
                      + 128         /* row residuals */
                      + 136;        /* flags (int) */
 
-template <bool KCA, bool KCB, bool FT>
+// Dynamic smem: [STAGES][A tile | B tile] (1024-byte aligned boxes for the 128-byte swizzle),
+// then [STAGES][w_J slice | v_I slice] (FT checksum vectors, BK each).  The FT epilogue
+// reuses the same bytes once the mainloop has drained.
+// Kernel modes.  NOFT: plain DGEMM (the overhead denominator; also computes the checksum
+// GEMMs of MODE_FT_PRE).  FT_PRE: the border of C^f = A^c B^r was
+// computed before the launch by two DMMA GEMMs, R = op(A) W and S^T = op(B)^T V^T (DESIGN.md
+// section 5, "checksum GEMMs"); the mainloop is the plain one and the epilogue verifies.
+// FT_FUSED: the checksum column / row are accumulated in the same mainloop from the operand
+// fragments (DFMA), as the paper fuses them into its kernel.
+enum { MODE_NOFT = 0, MODE_FT_PRE = 1, MODE_FT_FUSED = 2 };
+
+template <int MODE>
 struct SmemPlan {
-    static constexpr int A_EL = Tile<KCA>::ELEMS, B_EL = Tile<KCB>::ELEMS;
-    static constexpr int STAGE_EL = A_EL + B_EL + (FT ? 2 * BK : 0);
-    static constexpr int PIPE_EL = STAGES * STAGE_EL;
-    static constexpr int BYTES = 8 * ((FT && EPI_EL > PIPE_EL) ? EPI_EL : PIPE_EL);
+    static constexpr int STAGE_EL = 2 * TILE_EL;
+    static constexpr int PIPE_EL = STAGES * STAGE_EL + (MODE == MODE_FT_FUSED ? STAGES * 2 * BK : 0);
+    static constexpr int EL = (MODE != MODE_NOFT && EPI_EL > PIPE_EL) ? EPI_EL : PIPE_EL;
+    static constexpr int BYTES = 8 * EL + 1024;  // + alignment slack
 };
 
 // Tile rasterization: groups of GROUP_M tile-rows, column-major inside a group, so the
@@ -346,10 +471,12 @@ __device__ void warp_recompute(const GemmArgs &g, long long i, long long j, doub
     }
 }
 
-// Block = NTHREADS MMA threads (8 warps) + 1 producer warp that stages tiles with cp.async
-// and signals per-stage `full` mbarriers; MMA warps release stages through `empty` mbarriers
-// (no CTA-wide barrier in the mainloop, so the two MMA warps of an SMSP drift independently).
-constexpr int PRODUCER_THREADS = PRODUCER_THREADS_;  // one warpgroup; registers go to the MMA warps
+// Block = NTHREADS MMA threads (8 warps) + a producer warpgroup.  Thread 0 of the producer
+// issues the TMA boxes of each stage (and the bulk copies of the checksum-vector slices) and
+// arms the stage's `full` mbarrier with the byte count; MMA warps release stages through
+// `empty` mbarriers (no CTA-wide barrier in the mainloop).  The other producer threads only
+// work when an operand cannot be described by a tensor map (cp.async fallback) and, for FT,
+// reduce the threshold norms of the tile.
 constexpr int GEMM_THREADS = NTHREADS + PRODUCER_THREADS;
 // setmaxnreg only moves registers inside the CTA's launch allocation: ptxas caps a
 // __launch_bounds__(384, 1) kernel at 168 registers/thread (65536/384 rounded down to a
@@ -360,11 +487,22 @@ constexpr int MMA_REGS = 224, PRODUCER_REGS = 56;  // 256x224 + 128x56 = 64512
 static_assert(NTHREADS * MMA_REGS + PRODUCER_THREADS * PRODUCER_REGS <= GEMM_THREADS * LAUNCH_REGS,
               "setmaxnreg budget exceeds the launch register allocation (would deadlock)");
 
-template <bool KCA, bool KCB, bool VECA, bool VECB, bool FT>
-__global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmArgs g) {
-    extern __shared__ __align__(128) double smem[];
-    __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
-    using SP = SmemPlan<KCA, KCB, FT>;
+template <bool KCA, bool KCB, bool TMA, int MODE>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_kernel(const __grid_constant__ GemmArgs g, const __grid_constant__ CUtensorMap tmA,
+                const __grid_constant__ CUtensorMap tmB) {
+    extern __shared__ __align__(1024) double smem_raw[];
+    __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES], norm_bar;
+    // threshold norms of this tile (reading R4), reduced over the encode k-chunks by the
+    // producer warpgroup while the MMA warps run the mainloop
+    __shared__ double nrm_row[BM], nrm_col[BN], nrm_max[2];
+    // FT_PRE: this tile's slices of the checksum GEMM outputs R and S^T (loaded by the producer)
+    __shared__ double pre_r[MODE == MODE_FT_PRE ? BM : 1], pre_s[MODE == MODE_FT_PRE ? BN : 1];
+    constexpr bool FT = MODE != MODE_NOFT, FUSED = MODE == MODE_FT_FUSED;
+    constexpr bool TMA_A = TMA, TMA_B = TMA;
+    // 1024-byte aligned base, derived by indexing (keeps the pointer in the shared window so
+    // the loads below use 32-bit shared addressing)
+    double *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) / 8u;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp & 1, wn = warp >> 1;
     const long long ntm = (g.M + BM - 1) / BM, ntn = (g.N + BN - 1) / BN;
@@ -373,16 +511,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmArgs g) {
     const long long m0 = tm * BM, n0 = tn * BN;
     const int ktiles = (g.alpha == 0.0) ? 0 : (int)((g.K + BK - 1) / BK);
 
-    auto sA = [&](int st) { return smem + st * SP::STAGE_EL; };
-    auto sB = [&](int st) { return smem + st * SP::STAGE_EL + SP::A_EL; };
-    auto sW = [&](int st) { return smem + st * SP::STAGE_EL + SP::A_EL + SP::B_EL; };
-    auto sV = [&](int st) { return smem + st * SP::STAGE_EL + SP::A_EL + SP::B_EL + BK; };
+    auto sA = [&](int st) { return smem + st * SmemPlan<MODE>::STAGE_EL; };
+    auto sB = [&](int st) { return smem + st * SmemPlan<MODE>::STAGE_EL + TILE_EL; };
+    auto sW = [&](int st) { return smem + STAGES * SmemPlan<MODE>::STAGE_EL + st * 2 * BK; };
+    auto sV = [&](int st) { return sW(st) + BK; };
 
+    constexpr bool ALL_TMA = TMA_A && TMA_B;
     if (tid == 0) {
         for (int s = 0; s < STAGES; s++) {
-            mbar_init(&full_bar[s], PRODUCER_THREADS); // one cp.async arrival per producer thread
-            mbar_init(&empty_bar[s], NTHREADS / 32);   // one arrival per MMA warp
+            // thread 0 of the producer arrives with expect_tx; cp.async fallback threads add
+            // one arrival each when their copies land
+            mbar_init(&full_bar[s], 1 + (ALL_TMA ? 0 : PRODUCER_THREADS));
+            mbar_init(&empty_bar[s], NTHREADS / 32);  // one arrival per MMA warp
         }
+        mbar_init(&norm_bar, PRODUCER_THREADS);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
 
@@ -390,22 +533,58 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmArgs g) {
         // ------------------------------------------------------------ producer warpgroup
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
         const int pt = tid - NTHREADS;
-        for (int kt = 0; kt < ktiles; kt++) {
+        constexpr unsigned TX = (TMA_A ? TILE_EL * 8 : 0) + (TMA_B ? TILE_EL * 8 : 0) + (FUSED ? 2 * BK * 8 : 0);
+        auto produce = [&](int kt) {
             const int st = kt % STAGES;
-            if (kt >= STAGES) mbar_wait(&empty_bar[st], ((kt / STAGES) - 1) & 1);
             const long long k0 = (long long)kt * BK;
-            produce_tile<KCA, VECA>(sA(st), g.A, g.lda, m0, k0, g.M, g.K, pt);
-            produce_tile<KCB, VECB>(sB(st), g.B, g.ldb, n0, k0, g.N, g.K, pt);
-            if (FT) {
-#pragma unroll
-                for (int q = pt; q < BK; q += PRODUCER_THREADS) {
-                    if (q < BK / 2) cp_async16(sW(st) + q * 2, g.WB + tn * g.Kp + k0 + q * 2, 16);
-                    else            cp_async16(sV(st) + (q - BK / 2) * 2, g.VA + tm * g.Kp + k0 + (q - BK / 2) * 2, 16);
+            if (pt == 0) {
+                mbar_arrive_expect_tx(&full_bar[st], TX);
+                if (FUSED) {
+                    bulk_load(sW(st), g.WB + tn * g.Kp + k0, BK * 8, &full_bar[st]);
+                    bulk_load(sV(st), g.VA + tm * g.Kp + k0, BK * 8, &full_bar[st]);
                 }
             }
-            cp_async_mbar_arrive(&full_bar[st]);
+            produce_tile<KCA, TMA_A>(sA(st), &tmA, &full_bar[st], g.A, g.lda, m0, k0, g.M, g.K, pt);
+            produce_tile<KCB, TMA_B>(sB(st), &tmB, &full_bar[st], g.B, g.ldb, n0, k0, g.N, g.K, pt);
+            if (!ALL_TMA) cp_async_mbar_arrive(&full_bar[st]);
+        };
+        const int pro = ktiles < STAGES ? ktiles : STAGES;
+        for (int kt = 0; kt < pro; kt++) produce(kt);
+        if (FT) {
+            // norms for the verification thresholds: rows / columns of this tile, summed over
+            // the encode k-chunks in chunk order; tile maxima = max over chunks.  All loads of a
+            // thread are independent, so they are in flight together.
+            double ra = 0.0, cb = 0.0;
+            const long long gi = m0 + pt, gj = n0 + pt;
+            for (int c = 0; c < g.kch; c++) {
+                if (gi < g.M) ra += g.lineA[(long long)c * g.M + gi];
+                if (gj < g.N) cb += g.lineB[(long long)c * g.N + gj];
+            }
+            nrm_row[pt] = ra;
+            nrm_col[pt] = cb;
+            if (MODE == MODE_FT_PRE) {  // checksum GEMM outputs, k-split partials added in order
+                double r = 0.0, sv = 0.0;
+                if (gi < g.M)
+                    for (int q = 0; q < g.splits_r; q++) r += g.Rpre[q * g.stride_r + tn * g.M + gi];
+                if (gj < g.N)
+                    for (int q = 0; q < g.splits_s; q++) sv += g.Spre[q * g.stride_s + tm * g.N + gj];
+                pre_r[pt] = r;
+                pre_s[pt] = sv;
+            }
+            if (pt < 2) {
+                double mx = 0.0;
+                for (int c = 0; c < g.kch; c++)
+                    mx = fmax(mx, pt == 0 ? g.tmaxA[(long long)c * ntm + tm] : g.tmaxB[(long long)c * ntn + tn]);
+                nrm_max[pt] = mx;
+            }
+            mbar_arrive(&norm_bar);
         }
-        cp_wait<0>();
+        if (ALL_TMA && pt != 0) return;
+        for (int kt = STAGES; kt < ktiles; kt++) {
+            mbar_wait(&empty_bar[kt % STAGES], ((kt / STAGES) - 1) & 1);
+            produce(kt);
+        }
+        if (!ALL_TMA) cp_wait<0>();
         return;
     }
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(MMA_REGS));
@@ -415,79 +594,93 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmArgs g) {
     for (int a = 0; a < FM; a++)
 #pragma unroll
         for (int b = 0; b < FN; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
-    // checksum partials.  MN-contiguous smem layout: thread owns row/col (tid&127), k-half tid>>7.
-    // k-contiguous layout: warp w owns rows 16w..16w+15, lane (r=lane>>2, kk=lane&3) owns rows
-    // 16w+r and 16w+8+r at k = kk, kk+4, kk+8, kk+12 (2-wavefront smem reads).
-    double rp0 = 0.0, rp1 = 0.0, sp0 = 0.0, sp1 = 0.0;
+    // checksum partials (FT): the border of C^f = A^c B^r accumulated from
+    // the operand fragments already in registers for the DMMAs:
+    //   rp[t] += op(A)(row, k) w_J[k]   for the rows of A fragment 2 wn + t (column C e = A (B e))
+    //   sp[t] += v_I[k] op(B)(k, col)   for the cols of B fragment 2 wm + t (row e^T C = (e^T A) B)
+    // each lane over its k = 4 kk + (lane & 3); the 4 k-lanes are combined after the loop.  The
+    // four wn-warps of a wm-half split the 8 A fragments, the two wm-warps of a wn-column the 4 B
+    // fragments; the fragment is picked with warp-uniform selects (constant register indices).
+    double rp[2] = {0.0, 0.0}, sp[2] = {0.0, 0.0};
+    const FragAddr<KCA> fA(wm * WM, lane);
+    const FragAddr<KCB> fB(wn * WN, lane);
 
-    for (int kt = 0; kt < ktiles; kt++) {
-        const int st = kt % STAGES;
+    // One pipeline stage; `st` is a compile-time constant (the k-tile loop is unrolled by
+    // STAGES), so every fragment address is a per-thread offset plus an immediate.
+    auto consume = [&](const int st, const int kt) {
         mbar_wait(&full_bar[st], (kt / STAGES) & 1);
         const double *a_s = sA(st), *b_s = sB(st);
+        const double *w_s = sW(st), *v_s = sV(st);
 #pragma unroll
         for (int kk = 0; kk < BK / 4; kk++) {
             double af[FM], bf[FN];
             const int k = kk * 4 + (lane & 3);
 #pragma unroll
-            for (int f = 0; f < FM; f++) af[f] = a_s[Tile<KCA>::idx(wm * WM + f * 8 + (lane >> 2), k)];
+            for (int f = 0; f < FM; f++) af[f] = a_s[fA(f, kk)];
 #pragma unroll
-            for (int f = 0; f < FN; f++) bf[f] = b_s[Tile<KCB>::idx(wn * WN + f * 8 + (lane >> 2), k)];
+            for (int f = 0; f < FN; f++) bf[f] = b_s[fB(f, kk)];
 #pragma unroll
             for (int a = 0; a < FM; a++)
 #pragma unroll
                 for (int b = 0; b < FN; b++) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
-        }
-        if (FT) {
-            // checksum column r_i += sum_k op(A)(i,k) w_k  and row s_j += sum_k v_k op(B)(k,j)
-            const double *w_s = sW(st), *v_s = sV(st);
-            if (!KCA) {
-                const int r = tid & 127, h = tid >> 7;
-#pragma unroll
-                for (int q = 0; q < BK / 2; q++)
-                    rp0 = fma(a_s[Tile<KCA>::idx(r, h * (BK / 2) + q)], w_s[h * (BK / 2) + q], rp0);
-            } else {
-                const int r = warp * 16 + (lane >> 2), kk = lane & 3;
-#pragma unroll
-                for (int q = 0; q < BK / 4; q++) {
-                    rp0 = fma(a_s[Tile<KCA>::idx(r, kk + 4 * q)], w_s[kk + 4 * q], rp0);
-                    rp1 = fma(a_s[Tile<KCA>::idx(r + 8, kk + 4 * q)], w_s[kk + 4 * q], rp1);
-                }
-            }
-            if (!KCB) {
-                const int c = tid & 127, h = tid >> 7;
-#pragma unroll
-                for (int q = 0; q < BK / 2; q++)
-                    sp0 = fma(v_s[h * (BK / 2) + q], b_s[Tile<KCB>::idx(c, h * (BK / 2) + q)], sp0);
-            } else {
-                const int c = warp * 16 + (lane >> 2), kk = lane & 3;
-#pragma unroll
-                for (int q = 0; q < BK / 4; q++) {
-                    sp0 = fma(v_s[kk + 4 * q], b_s[Tile<KCB>::idx(c, kk + 4 * q)], sp0);
-                    sp1 = fma(v_s[kk + 4 * q], b_s[Tile<KCB>::idx(c + 8, kk + 4 * q)], sp1);
-                }
+            if (FUSED) {
+                const double wk = w_s[k], vk = v_s[k];
+                // warp-uniform branches pick the fragment pair (no select temporaries)
+                if (wn == 0)      { rp[0] = fma(af[0], wk, rp[0]); rp[1] = fma(af[1], wk, rp[1]); }
+                else if (wn == 1) { rp[0] = fma(af[2], wk, rp[0]); rp[1] = fma(af[3], wk, rp[1]); }
+                else if (wn == 2) { rp[0] = fma(af[4], wk, rp[0]); rp[1] = fma(af[5], wk, rp[1]); }
+                else              { rp[0] = fma(af[6], wk, rp[0]); rp[1] = fma(af[7], wk, rp[1]); }
+                if (wm == 0) { sp[0] = fma(vk, bf[0], sp[0]); sp[1] = fma(vk, bf[1], sp[1]); }
+                else         { sp[0] = fma(vk, bf[2], sp[0]); sp[1] = fma(vk, bf[3], sp[1]); }
             }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[st]);
+    };
+    for (int kt0 = 0; kt0 < ktiles; kt0 += STAGES) {
+#pragma unroll
+        for (int st = 0; st < STAGES; st++)
+            if (kt0 + st < ktiles) consume(st, kt0 + st);
     }
-    bar_mma();  // all MMA warps done with the pipeline smem (the producer has no pending copies)
+    bar_mma();  // all MMA warps done with the pipeline smem (every issued copy was consumed)
+
+    // accumulator element (a, b, e) of this thread is C-tile entry (row_of(a), col_of(b, e))
+    auto row_of = [&](int a) { return frag_mn<KCA>(wm * WM, a, lane >> 2); };
+    auto col_of = [&](int b, int e) { return frag_mn<KCB>(wn * WN, b, 2 * (lane & 3) + e); };
 
     const bool beta0 = (g.beta == 0.0);
     if (!FT) {
         // ---------------------------------------------------------- non-FT epilogue
-#pragma unroll
-        for (int a = 0; a < FM; a++)
+        // Straight from the accumulator fragments: for fixed (a, b, e) a warp writes 4 columns
+        // x 8 rows (full 32-byte sectors).  C0 is software-pipelined by fragment row-group: the
+        // loads of group a+1 are issued before the stores of group a (different addresses), so
+        // two groups of independent loads are in flight.
+        auto load_c0 = [&](int a, double (&c0)[FN][2]) {
+            const long long gi = m0 + row_of(a);
 #pragma unroll
             for (int b = 0; b < FN; b++)
 #pragma unroll
                 for (int e = 0; e < 2; e++) {
-                    const long long gi = m0 + wm * WM + a * 8 + (lane >> 2);
-                    const long long gj = n0 + wn * WN + b * 8 + 2 * (lane & 3) + e;
-                    if (gi < g.M && gj < g.N) {
-                        double *p = g.C + gi + gj * g.ldc;
-                        *p = beta0 ? g.alpha * acc[a][b][e] : fma(g.alpha, acc[a][b][e], g.beta * *p);
-                    }
+                    const long long gj = n0 + col_of(b, e);
+                    c0[b][e] = (!beta0 && gi < g.M && gj < g.N) ? __ldcs(g.C + gi + gj * g.ldc) : 0.0;
                 }
+        };
+        double c0[2][FN][2];
+        load_c0(0, c0[0]);
+#pragma unroll
+        for (int a = 0; a < FM; a++) {
+            if (a + 1 < FM) load_c0(a + 1, c0[(a + 1) & 1]);
+            const long long gi = m0 + row_of(a);
+#pragma unroll
+            for (int b = 0; b < FN; b++)
+#pragma unroll
+                for (int e = 0; e < 2; e++) {
+                    const long long gj = n0 + col_of(b, e);
+                    if (gi < g.M && gj < g.N)
+                        g.C[gi + gj * g.ldc] =
+                            beta0 ? g.alpha * acc[a][b][e] : fma(g.alpha, acc[a][b][e], g.beta * c0[a & 1][b][e]);
+                }
+        }
         return;
     }
 
@@ -500,31 +693,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmArgs g) {
     int *flags = reinterpret_cast<int *>(dres + 128);  // [0] nrow, [1] ncol, [2..129] rows, [130..257] cols
     const long long mvalid = min((long long)BM, g.M - m0), nvalid = min((long long)BN, g.N - n0);
 
-    // checksum partials -> rsp/ssp ([2][128]: r_i = rsp[i] + rsp[128+i])
-    if (!KCA) {
-        rsp[tid] = rp0;
-    } else {
+    // checksum reference: FUSED -- combine the 4 k-lanes of the mainloop partials (fixed order),
+    // one writer per row / column; FT_PRE -- the checksum-GEMM slices staged by the producer
+    // (read after the norm barrier below).  rsp[i] = r_i (row i of the C e column), ssp[j] = s_j
+    // (column j of the e^T C row).
+    if (FUSED) {
 #pragma unroll
-        for (int off = 1; off <= 2; off <<= 1) {
-            rp0 += __shfl_xor_sync(0xffffffffu, rp0, off);
-            rp1 += __shfl_xor_sync(0xffffffffu, rp1, off);
+        for (int t = 0; t < 2; t++) {
+            rp[t] += __shfl_xor_sync(0xffffffffu, rp[t], 1);
+            rp[t] += __shfl_xor_sync(0xffffffffu, rp[t], 2);
+            sp[t] += __shfl_xor_sync(0xffffffffu, sp[t], 1);
+            sp[t] += __shfl_xor_sync(0xffffffffu, sp[t], 2);
         }
         if ((lane & 3) == 0) {
-            const int r = warp * 16 + (lane >> 2);
-            rsp[r] = rp0; rsp[r + 8] = rp1; rsp[128 + r] = 0.0; rsp[128 + r + 8] = 0.0;
-        }
-    }
-    if (!KCB) {
-        ssp[tid] = sp0;
-    } else {
 #pragma unroll
-        for (int off = 1; off <= 2; off <<= 1) {
-            sp0 += __shfl_xor_sync(0xffffffffu, sp0, off);
-            sp1 += __shfl_xor_sync(0xffffffffu, sp1, off);
-        }
-        if ((lane & 3) == 0) {
-            const int c = warp * 16 + (lane >> 2);
-            ssp[c] = sp0; ssp[c + 8] = sp1; ssp[128 + c] = 0.0; ssp[128 + c + 8] = 0.0;
+            for (int t = 0; t < 2; t++) {
+                rsp[frag_mn<KCA>(wm * WM, 2 * wn + t, lane >> 2)] = rp[t];
+                ssp[frag_mn<KCB>(wn * WN, 2 * wm + t, lane >> 2)] = sp[t];
+            }
         }
     }
     if (tid == 0) { flags[0] = 0; flags[1] = 0; }
@@ -532,11 +718,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmArgs g) {
     // C0 tile -> smem, then its row/column sums (the beta C encoding)
     const int rr = tid & 127, hh = tid >> 7;
     if (!beta0) {
-        for (int idx = tid; idx < BM * BN; idx += NTHREADS) {
-            const int row = idx & 127, col = idx >> 7;
-            const long long gi = m0 + row, gj = n0 + col;
-            tileS[row + col * LDT] = (gi < g.M && gj < g.N) ? g.C[gi + gj * g.ldc] : 0.0;
+        // C0 tile -> smem with cp.async: every load of the tile is in flight at once
+        // (zero-fill outside M x N)
+        if (g.vecC) {
+#pragma unroll 8
+            for (int idx = tid; idx < BM * BN / 2; idx += NTHREADS) {
+                const int row = (idx & 63) * 2, col = idx >> 6;
+                const long long gi = m0 + row, gj = n0 + col;
+                const int nv = (gj < g.N) ? (int)min(2ll, max(0ll, g.M - gi)) : 0;
+                cp_async16(tileS + row + col * LDT, nv ? g.C + gi + gj * g.ldc : g.C, nv * 8);
+            }
+        } else {
+#pragma unroll 8
+            for (int idx = tid; idx < BM * BN; idx += NTHREADS) {
+                const int row = idx & 127, col = idx >> 7;
+                const long long gi = m0 + row, gj = n0 + col;
+                const bool ok = gi < g.M && gj < g.N;
+                cp_async8(tileS + row + col * LDT, ok ? g.C + gi + gj * g.ldc : g.C, ok ? 8 : 0);
+            }
         }
+        cp_commit();
+        cp_wait<0>();
         bar_mma();
         double s = 0.0, sa = 0.0;
         for (int c = hh * 64; c < hh * 64 + 64; c++) {
@@ -574,8 +776,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmArgs g) {
                 for (int b = 0; b < FN; b++)
 #pragma unroll
                     for (int e = 0; e < 2; e++) {
-                        const int row = wm * WM + a * 8 + (lane >> 2), col = wn * WN + b * 8 + 2 * (lane & 3) + e;
-                        if (row == li && col == lj) acc[a][b][e] = flip_bit(acc[a][b][e], bit);
+                        if (row_of(a) == li && col_of(b, e) == lj) acc[a][b][e] = flip_bit(acc[a][b][e], bit);
                     }
         }
     }
@@ -586,7 +787,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmArgs g) {
         for (int b = 0; b < FN; b++)
 #pragma unroll
             for (int e = 0; e < 2; e++) {
-                const int row = wm * WM + a * 8 + (lane >> 2), col = wn * WN + b * 8 + 2 * (lane & 3) + e;
+                const int row = row_of(a), col = col_of(b, e);
                 const bool ok = row < mvalid && col < nvalid;
                 double o;
                 if (beta0) o = g.alpha * acc[a][b][e];
@@ -612,20 +813,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmArgs g) {
     bar_mma();
     // verification: flag rows / columns beyond the round-off threshold
     const double aa = fabs(g.alpha), ab = fabs(g.beta);
+    mbar_wait(&norm_bar, 0);  // producer-reduced norms are in nrm_row / nrm_col / nrm_max
     if (tid < 128) {
         const int r = tid;
-        const long long gi = m0 + r;
         if (r < mvalid) {
             const double sum = rowS[r] + rowS[128 + r];
-            const double rr2 = rsp[r] + rsp[128 + r];
+            const double rr2 = FUSED ? rsp[r] : pre_r[r];
             const double c0s = beta0 ? 0.0 : rowC[r] + rowC[128 + r];
             const double c0a = beta0 ? 0.0 : rowCA[r] + rowCA[128 + r];
             const double ref = beta0 ? g.alpha * rr2 : fma(g.alpha, rr2, g.beta * c0s);
-            double rowabs = 0.0, bmax = 0.0;
-            for (int c = 0; c < g.kch; c++) {
-                rowabs += g.lineA[(long long)c * g.M + gi];
-                bmax = fmax(bmax, g.tmaxB[(long long)c * ntn + tn]);
-            }
+            const double rowabs = nrm_row[r], bmax = nrm_max[1];
             const double tau = 4.0 * U_ROUND * (double)(g.K + nvalid + 3) * (aa * rowabs * bmax + ab * c0a);
             const double d = sum - ref;
             dres[r] = d;
@@ -636,18 +833,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmArgs g) {
         }
     } else {
         const int c = tid - 128;
-        const long long gj = n0 + c;
         if (c < nvalid) {
             const double sum = colS[c];
-            const double ss2 = ssp[c] + ssp[128 + c];
+            const double ss2 = FUSED ? ssp[c] : pre_s[c];
             const double c0s = beta0 ? 0.0 : colC[c];
             const double c0a = beta0 ? 0.0 : colCA[c];
             const double ref = beta0 ? g.alpha * ss2 : fma(g.alpha, ss2, g.beta * c0s);
-            double colabs = 0.0, amax = 0.0;
-            for (int q = 0; q < g.kch; q++) {
-                colabs += g.lineB[(long long)q * g.N + gj];
-                amax = fmax(amax, g.tmaxA[(long long)q * ntm + tm]);
-            }
+            const double colabs = nrm_col[c], amax = nrm_max[0];
             const double tau = 4.0 * U_ROUND * (double)(g.K + mvalid + 3) * (aa * amax * colabs + ab * c0a);
             const double d = sum - ref;
             if (!(fabs(d) <= tau)) {
@@ -704,6 +896,117 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmArgs g) {
     for (int idx = tid; idx < BM * BN; idx += NTHREADS) {
         const int row = idx & 127, col = idx >> 7;
         if (row < mvalid && col < nvalid) g.C[(m0 + row) + (n0 + col) * g.ldc] = tileS[row + col * LDT];
+    }
+}
+
+
+// ------------------------------------------------------------------ checksum GEMM kernel
+// The checksum GEMMs of MODE_FT_PRE (the border of C^f = A^c B^r):
+//   R   (M x ntn) = op(A)   . [B e_J]_J        (C e for every column tile J)
+//   S^T (N x ntm) = op(B)^T . [(e_I^T A)^T]_I  (e^T C for every row tile I)
+// i.e. out (P x Q) = X (P x K) . Y (K x Q) with Q = ntn or ntm small and Y = the encode
+// vectors (k-contiguous, ld Kp).  A CTA computes 128 rows of P times all QN (>= Q) columns
+// over one k-split; split s writes its partial to out + s * split_stride (no atomics: the
+// FT_PRE epilogue adds the splits in order, so the result is deterministic).  Same producer /
+// TMA / swizzled-fragment machinery as gemm_kernel; warp w owns rows 16w..16w+15 (2 DMMA
+// row fragments) x QN/8 column fragments.
+struct CkArgs {
+    const double *X, *Y;
+    long long ldx, ldy;
+    long long P, Q, K, kper;  // kper: k per split (multiple of BK)
+    double *out;
+    long long ldo, split_stride;
+};
+
+template <int QN>
+struct CkPlan {
+    static constexpr int B_EL = QN * BK;
+    static constexpr int STAGE_EL = TILE_EL + B_EL;
+    static constexpr int BYTES = 8 * STAGES * STAGE_EL + 1024;
+};
+
+template <bool KCX, bool TMA, int QN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    cksum_kernel(const __grid_constant__ CkArgs g, const __grid_constant__ CUtensorMap tmX,
+                 const __grid_constant__ CUtensorMap tmY) {
+    constexpr int FQ = QN / 8;
+    extern __shared__ __align__(1024) double smem_raw[];
+    __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
+    double *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) / 8u;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long p0 = (long long)blockIdx.x * BM;
+    const long long kbeg = (long long)blockIdx.y * g.kper;
+    const long long kend = min(g.K, kbeg + g.kper);
+    const int ktiles = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+    auto sX = [&](int st) { return smem + st * CkPlan<QN>::STAGE_EL; };
+    auto sY = [&](int st) { return smem + st * CkPlan<QN>::STAGE_EL + TILE_EL; };
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&full_bar[s], 1 + (TMA ? 0 : PRODUCER_THREADS));
+            mbar_init(&empty_bar[s], NTHREADS / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (warp >= NTHREADS / 32) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
+        const int pt = tid - NTHREADS;
+        constexpr unsigned TX = TMA ? (TILE_EL + CkPlan<QN>::B_EL) * 8 : 0;
+        for (int kt = 0; kt < ktiles; kt++) {
+            const int st = kt % STAGES;
+            if (kt >= STAGES) mbar_wait(&empty_bar[st], ((kt / STAGES) - 1) & 1);
+            const long long k0 = kbeg + (long long)kt * BK;
+            if (pt == 0) mbar_arrive_expect_tx(&full_bar[st], TX);
+            produce_tile<KCX, TMA>(sX(st), &tmX, &full_bar[st], g.X, g.ldx, p0, k0, g.P, g.K, pt);
+            produce_tile<true, TMA, QN>(sY(st), &tmY, &full_bar[st], g.Y, g.ldy, 0, k0, g.Q, g.K, pt);
+            if (!TMA) cp_async_mbar_arrive(&full_bar[st]);
+            if (TMA && pt != 0) break;  // thread 0 issues every TMA stage
+        }
+        if (!TMA) cp_wait<0>();
+        return;
+    }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(MMA_REGS));
+    double acc[2][FQ][2];
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < FQ; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+    const FragAddr<KCX> fX(warp * 16, lane);
+    const FragAddr<true, QN> fY(0, lane);
+    auto consume = [&](const int st, const int kt) {
+        mbar_wait(&full_bar[st], (kt / STAGES) & 1);
+        const double *x_s = sX(st), *y_s = sY(st);
+#pragma unroll
+        for (int kk = 0; kk < BK / 4; kk++) {
+            double xf[2], yf[FQ];
+#pragma unroll
+            for (int f = 0; f < 2; f++) xf[f] = x_s[fX(f, kk)];
+#pragma unroll
+            for (int f = 0; f < FQ; f++) yf[f] = y_s[fY(f, kk)];
+#pragma unroll
+            for (int a = 0; a < 2; a++)
+#pragma unroll
+                for (int b = 0; b < FQ; b++) dmma(acc[a][b][0], acc[a][b][1], xf[a], yf[b]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[st]);
+    };
+    for (int kt0 = 0; kt0 < ktiles; kt0 += STAGES) {
+#pragma unroll
+        for (int st = 0; st < STAGES; st++)
+            if (kt0 + st < ktiles) consume(st, kt0 + st);
+    }
+    double *out = g.out + (long long)blockIdx.y * g.split_stride;
+#pragma unroll
+    for (int a = 0; a < 2; a++) {
+        const long long pi = p0 + frag_mn<KCX>(warp * 16, a, lane >> 2);
+#pragma unroll
+        for (int b = 0; b < FQ; b++)
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+                const long long q = 8 * b + 2 * (lane & 3) + e;
+                if (pi < g.P && q < g.Q) out[pi + q * g.ldo] = acc[a][b][e];
+            }
     }
 }
 

@@ -66,6 +66,10 @@ def _load():
     L.ftblas_last_error.restype = ct.c_char_p
     L.ftblas_release.argtypes = []
     L.ftblas_release.restype = ct.c_int
+    L.ftblas_set_checksum_mode.argtypes = [ct.c_int]
+    L.ftblas_set_checksum_mode.restype = ct.c_int
+    L.ftblas_get_checksum_mode.argtypes = []
+    L.ftblas_get_checksum_mode.restype = ct.c_int
     return L
 
 
@@ -75,7 +79,11 @@ lib = _load()
 EXPORTS = ("ftblas_dgemm", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_report_fetch",
            "ftblas_set_fault_plan", "ftblas_set_stream", "ftblas_launch_count",
            "ftblas_tile_shape", "ftblas_last_error", "ftblas_release", "ftblas_profile",
-           "ftblas_profile_read")
+           "ftblas_profile_read", "ftblas_set_checksum_mode", "ftblas_get_checksum_mode")
+
+CHECKSUM_GEMM = 0   # FTBLAS_CHECKSUM_GEMM: checksum row/column by two DMMA GEMMs (default)
+CHECKSUM_FUSED = 1  # FTBLAS_CHECKSUM_FUSED: accumulated in the main GEMM's mainloop
+CHECKSUM_MODES = {"gemm": CHECKSUM_GEMM, "fused": CHECKSUM_FUSED}
 
 
 def _ptr(x):
@@ -166,6 +174,15 @@ def ftblas_set_fault_plan(i, j, bit):
 
 def ftblas_clear_fault_plan():
     _check(lib.ftblas_set_fault_plan(0, None, None, None))
+
+
+def ftblas_set_checksum_mode(mode):
+    """mode: CHECKSUM_GEMM / CHECKSUM_FUSED or the names 'gemm' / 'fused'."""
+    _check(lib.ftblas_set_checksum_mode(CHECKSUM_MODES.get(mode, mode)))
+
+
+def ftblas_get_checksum_mode() -> int:
+    return lib.ftblas_get_checksum_mode()
 
 
 def ftblas_set_stream(stream):

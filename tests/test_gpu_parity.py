@@ -16,14 +16,28 @@ from tests._util import from_dev, gemm_bound, report_key, to_dev
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def ft():
+def _lib(mode):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2305_02444_b200 import ftblas
     ftblas.ftblas_set_stream(None)
+    ftblas.ftblas_set_checksum_mode(mode)
     return ftblas
+
+
+@pytest.fixture(params=["gemm", "fused"])
+def ft(request):
+    """The library in each checksum mode (checksum GEMMs / fused mainloop checksums)."""
+    lib = _lib(request.param)
+    yield lib
+    lib.ftblas_set_checksum_mode("gemm")
+
+
+@pytest.fixture
+def ftd():
+    """The library in its default checksum mode (full-size configs)."""
+    return _lib("gemm")
 
 
 def run_gpu(ft, w, d, *, plan=None, noft=False, offsets=(0, 0, 0)):
@@ -83,6 +97,9 @@ SMALL = [
     (1, 1, 1, "N", "N", 2.0, 0.0, "uniform", 0),
     (5, 700, 9, "N", "T", 1.0, 1.0, "normal", 1),
     (700, 3, 17, "T", "N", 1.0, 0.0, "uniform", 0),
+    # more than 128 verification tiles along N / M: checksum GEMMs in several column blocks
+    (200, 16512, 40, "N", "T", 1.0, 0.5, "uniform", 0),
+    (16600, 130, 40, "T", "N", -1.0, 0.0, "normal", 0),
 ]
 
 
@@ -195,11 +212,11 @@ def test_host_buffer_entry_point(ft):
 
 
 # ---------------------------------------------------------------- BASELINE configs
-def test_config0_all_flips_corrected(ft):
+def test_config0_all_flips_corrected(ftd):
     w = syn.CONFIGS[0]
     d = syn.make_inputs(w)
     plan = syn.fault_plan(w.M, w.N, w.n_flips, w.seed)
-    C_gpu, rep = run_gpu(ft, w, d, plan=plan)
+    C_gpu, rep = run_gpu(ftd, w, d, plan=plan)
     C_ref, orep, st = run_oracle(w, d, plan)
     assert rep.count == st.count == w.n_flips
     assert report_key(rep.entries()) == report_key(orep)
@@ -263,13 +280,13 @@ def check_full_config(ft, w, oracle_tiles=None):
     sampled_check(w, d, C_gpu, n=100, seed=1, extra=list(zip(plan[0].tolist(), plan[1].tolist()))[:50])
 
 
-def test_config1_4096_tn(ft):
-    check_full_config(ft, syn.CONFIGS[1], oracle_tiles=100)
+def test_config1_4096_tn(ftd):
+    check_full_config(ftd, syn.CONFIGS[1], oracle_tiles=100)
 
 
-def test_config2_rank_k_update(ft):
-    check_full_config(ft, syn.CONFIGS[2], oracle_tiles=32)
+def test_config2_rank_k_update(ftd):
+    check_full_config(ftd, syn.CONFIGS[2], oracle_tiles=32)
 
 
-def test_config3_16384(ft):
-    check_full_config(ft, syn.CONFIGS[3], oracle_tiles=6)
+def test_config3_16384(ftd):
+    check_full_config(ftd, syn.CONFIGS[3], oracle_tiles=6)
