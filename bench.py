@@ -194,6 +194,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
     fb.ftblas_set_stream(stream)
+    fb.ftblas_set_checksum_mode("gemm")
 
     def barrier():
         if world > 1:
@@ -288,6 +289,11 @@ def main():
         fb.ftblas_clear_fault_plan()
         ms_ft0 = timed(lambda: step(gemm_ft, False), K)
         ms_noft = timed(lambda: step(gemm_noft, False), K)
+        # the same FT call with the checksum row/column accumulated in the main mainloop
+        # (FTBLAS_CHECKSUM_FUSED) instead of the checksum GEMMs, for comparison
+        fb.ftblas_set_checksum_mode("fused")
+        ms_fused0 = timed(lambda: step(gemm_ft, False), max(1, min(K, 3)))
+        fb.ftblas_set_checksum_mode("gemm")
         for _ in range(2):  # keep the GPU loaded until the sampler stops
             step(gemm_ft, False)
         torch.cuda.synchronize()
@@ -370,12 +376,16 @@ def main():
             "noft_tflops": tf(ms_noft), "ft_0err_tflops": tf(ms_ft0), "ft_flips_tflops": tf(ms_ft_err),
             "ft_overhead_pct": {"errors_0": 100.0 * (ms_ft0 / ms_noft - 1.0),
                                 f"errors_{w.n_flips}": 100.0 * (ms_ft_err / ms_noft - 1.0)},
+            "checksum_mode": "gemm (checksum row/column by split-K DMMA GEMMs before the main GEMM)",
+            "fused_mode": {"ft_0err_tflops": tf(ms_fused0), "ft_overhead_pct": 100.0 * (ms_fused0 / ms_noft - 1.0),
+                           "note": "checksums accumulated in the main mainloop (DFMA beside DMMA)"},
             "corrections": {"planned": int(len(plan[0])), "reported": reported, "all_located_and_corrected": bool(ok_all)},
             "gpu_launches": launches_all,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                         "kernel": "gemm_kernel<FT> (DMMA + fused ABFT)", "kernel_ms": gemm_avg_ms,
-                         "encode_kernel_ms": enc_avg_ms,
+                         "kernel": "gemm_kernel<FT_PRE> (TMA + DMMA mainloop, verify/locate/correct epilogue)",
+                         "kernel_ms": gemm_avg_ms,
+                         "checksum_stage_ms": enc_avg_ms,
                          "peak_source": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DMMA microbench 37.15, profiles/r01_fp64_pipes.txt)"},
             "clocks": clocks,
             "e2e": e2e,

@@ -345,12 +345,11 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
     }
     if (ft) {
         const long long Kp = std::max<long long>(BK, (K + BK - 1) / BK * BK);
-        // k-chunks of the encode pass: enough blocks to fill the GPU, chunks >= 32 columns
-        // k-chunks of the encode pass: ~1024 k per block (1 MiB slabs for 128-wide tiles), at
-        // least two blocks per SM in total, chunks >= 32 columns, at most 16 partials per row
-        // (the GEMM producer reduces them per tile)
-        long long kch_l = std::max<long long>((Kp + 1023) / 1024, (2 * 148 + ntm + ntn - 1) / (ntm + ntn));
-        kch_l = std::min<long long>({kch_l, 16, std::max<long long>(1, Kp / 32)});
+        // k-chunks of the encode pass: about eight waves of blocks (two resident per SM), so the
+        // last partial wave costs little; chunks >= 128 columns; at most 32 partials per row (the
+        // GEMM producer reduces them per tile)
+        long long kch_l = (8 * 2 * 148 + ntm + ntn - 1) / (ntm + ntn);
+        kch_l = std::min<long long>({kch_l, 32, std::max<long long>(1, Kp / 128)});
         int kch = (int)std::max<long long>(1, kch_l);
         const long long kper = ((Kp + kch - 1) / kch + 31) / 32 * 32;
         const size_t nV = (size_t)(ntm + ntn) * Kp, nLine = (size_t)kch * (M + N), nT = (size_t)kch * (ntm + ntn);

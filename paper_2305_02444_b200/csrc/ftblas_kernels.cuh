@@ -44,8 +44,8 @@ constexpr double U_ROUND = 1.0 / 9007199254740992.0;  // 2^-53
 //            [128 mn-rows][16 k].
 // Inside 128-byte row r, the 16-byte unit u (elements 2u, 2u+1) sits at unit u ^ (r & 7).
 // With the fragment row maps of frag_mn() below, every DMMA fragment load (a warp reads
-// 8 mn x 4 k) and every checksum load touches each 8-byte bank pair exactly twice: 2
-// wavefronts for 256 bytes, i.e. conflict-free.
+// 8 mn x 4 k; the 64-bit shared load is served per half-warp of 4 mn x 4 k) touches 16
+// distinct 8-byte bank pairs in each half-warp: 2 wavefronts for 256 bytes, conflict-free.
 // (ROWS = mn extent of the tile: 128 for the main GEMM, 16..128 for the checksum GEMMs' thin
 // operand.)
 constexpr int TILE_EL = 128 * BK;
@@ -61,15 +61,19 @@ struct Tile {
         }
     }
 };
-// mn index (within the CTA tile) of row g (0..7) of the 8-wide fragment f of a warp tile
-// starting at `base`.  KC=true: natural order.  KC=false: fragment f takes mn
-// {4(f&1)+0..3, 4(f&1)+8..11} of the 16-mn box f/2, which spreads its 8 rows over 4
-// distinct 16-byte units of every swizzled k-row (see Tile).  The accumulator row / column
-// of C fragment element (g, j) is frag_mn of the A / B side: the MMA is agnostic to which
-// mn a fragment row stands for, as long as A, B and C agree.
+// mn index (within the CTA tile) of row g = (g2 g1 g0) of the 8-wide fragment f of a warp
+// tile starting at `base` (a half-warp has fixed g2 and covers g0, g1 x 4 k):
+//   KC=true : mn = base + 8 f + (g2 + 2 g0 + 4 g1)     -> bank pair (k0, k1^g2, k2^g0, k3^g1)
+//   KC=false: mn = base + 16 (f>>1) + (g0 + 2 (f&1) + 4 g2 + 8 g1)
+//                                                       -> bank pair (g0, f1^k0, g2^k1, g1^k2)
+// so the 16 lanes of a half-warp hit 16 distinct bank pairs in both layouts.  The
+// accumulator row / column of C fragment element (g, j) is frag_mn of the A / B side: the
+// MMA is agnostic to which mn a fragment row stands for, as long as A, B and C agree.
 template <bool KC>
 __device__ __forceinline__ int frag_mn(int base, int f, int g) {
-    return KC ? base + 8 * f + g : base + 16 * (f >> 1) + 4 * (f & 1) + (g & 3) + 8 * (g >> 2);
+    const int g0 = g & 1, g1 = (g >> 1) & 1, g2 = g >> 2;
+    return KC ? base + 8 * f + (g2 + 2 * g0 + 4 * g1)
+              : base + 16 * (f >> 1) + (g0 + 2 * (f & 1) + 4 * g2 + 8 * g1);
 }
 
 // Per-thread precomputed smem offsets of the DMMA fragment loads: the element (row g of
@@ -84,12 +88,12 @@ struct FragAddr {
         const int g = lane >> 2, l3 = lane & 3;
 #pragma unroll
         for (int v = 0; v < 4; v++) {
-            if (KC) {  // v = kk & 3; mn = base + 8 f + g, (mn & 7) = g since base % 8 == 0
-                const int kk16 = 4 * v + l3;
-                off[v] = (base + g) * 16 + ((((kk16 >> 1) ^ g) << 1) | (kk16 & 1));
+            if (KC) {  // v = kk & 3; mn = base + frag_mn<true>(0, 0, g), base % 8 == 0
+                const int kk16 = 4 * v + l3, n = frag_mn<true>(0, 0, g);
+                off[v] = (base + n) * 16 + ((((kk16 >> 1) ^ (n & 7)) << 1) | (kk16 & 1));
             } else {   // v = (f & 1) | (kk & 1) << 1; base % 16 == 0
                 const int f1 = v & 1, k7 = 4 * (v >> 1) + l3;
-                const int m = 4 * f1 + (g & 3) + 8 * (g >> 2);
+                const int m = frag_mn<false>(0, f1, g);
                 off[v] = (base >> 4) * (BK * 16) + l3 * 16 + ((((m >> 1) ^ k7) << 1) | (m & 1));
             }
         }
@@ -440,6 +444,31 @@ struct SmemPlan {
     static constexpr int BYTES = 8 * EL + 1024;  // + alignment slack
 };
 
+// sum_{c < n} p[c * stride] in index order, loads issued in batches of 8 (n <= 64 here)
+__device__ __forceinline__ double sum_strided(const double *p, long long stride, int n) {
+    double s = 0.0;
+    for (int c0 = 0; c0 < n; c0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) v[u] = (c0 + u < n) ? p[(long long)(c0 + u) * stride] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+            if (c0 + u < n) s += v[u];
+    }
+    return s;
+}
+__device__ __forceinline__ double max_strided(const double *p, long long stride, int n) {
+    double m = 0.0;
+    for (int c0 = 0; c0 < n; c0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) v[u] = (c0 + u < n) ? p[(long long)(c0 + u) * stride] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; u++) m = fmax(m, v[u]);
+    }
+    return m;
+}
+
 // Tile rasterization: groups of GROUP_M tile-rows, column-major inside a group, so the
 // CTAs resident at one time share a few A row panels and B column panels in L2.
 constexpr int GROUP_M = 16;
@@ -524,7 +553,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             mbar_init(&full_bar[s], 1 + (ALL_TMA ? 0 : PRODUCER_THREADS));
             mbar_init(&empty_bar[s], NTHREADS / 32);  // one arrival per MMA warp
         }
-        mbar_init(&norm_bar, PRODUCER_THREADS);
+        mbar_init(&norm_bar, PRODUCER_THREADS - 32);  // producer warps 1..3
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -548,43 +577,45 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             produce_tile<KCB, TMA_B>(sB(st), &tmB, &full_bar[st], g.B, g.ldb, n0, k0, g.N, g.K, pt);
             if (!ALL_TMA) cp_async_mbar_arrive(&full_bar[st]);
         };
-        const int pro = ktiles < STAGES ? ktiles : STAGES;
-        for (int kt = 0; kt < pro; kt++) produce(kt);
-        if (FT) {
-            // norms for the verification thresholds: rows / columns of this tile, summed over
-            // the encode k-chunks in chunk order; tile maxima = max over chunks.  All loads of a
-            // thread are independent, so they are in flight together.
-            double ra = 0.0, cb = 0.0;
-            const long long gi = m0 + pt, gj = n0 + pt;
-            for (int c = 0; c < g.kch; c++) {
-                if (gi < g.M) ra += g.lineA[(long long)c * g.M + gi];
-                if (gj < g.N) cb += g.lineB[(long long)c * g.N + gj];
-            }
-            nrm_row[pt] = ra;
-            nrm_col[pt] = cb;
-            if (MODE == MODE_FT_PRE) {  // checksum GEMM outputs, k-split partials added in order
-                double r = 0.0, sv = 0.0;
-                if (gi < g.M)
-                    for (int q = 0; q < g.splits_r; q++) r += g.Rpre[q * g.stride_r + tn * g.M + gi];
-                if (gj < g.N)
-                    for (int q = 0; q < g.splits_s; q++) sv += g.Spre[q * g.stride_s + tm * g.N + gj];
-                pre_r[pt] = r;
-                pre_s[pt] = sv;
-            }
-            if (pt < 2) {
-                double mx = 0.0;
-                for (int c = 0; c < g.kch; c++)
-                    mx = fmax(mx, pt == 0 ? g.tmaxA[(long long)c * ntm + tm] : g.tmaxB[(long long)c * ntn + tn]);
-                nrm_max[pt] = mx;
+        if (FT && pt >= 32) {
+            // Threshold norms (reading R4) and, for FT_PRE, the checksum-GEMM slices of this tile,
+            // by producer warps 1..3 while thread 0 streams the operand stages: quantity q < 128 is
+            // row q, 128 <= q < 256 column q - 128, 256 / 257 the tile maxima of A / B.  Sums over
+            // the encode k-chunks / the k-splits in fixed order, loads issued in batches.
+            for (int q = pt - 32; q < 2 * 128 + 2; q += PRODUCER_THREADS - 32) {
+                if (q < 128) {
+                    const long long gi = m0 + q;
+                    const bool ok = gi < g.M;
+                    nrm_row[q] = ok ? sum_strided(g.lineA + gi, g.M, g.kch) : 0.0;
+                    if (MODE == MODE_FT_PRE)
+                        pre_r[q] = ok ? sum_strided(g.Rpre + tn * g.M + gi, g.stride_r, g.splits_r) : 0.0;
+                } else if (q < 256) {
+                    const long long gj = n0 + (q - 128);
+                    const bool ok = gj < g.N;
+                    nrm_col[q - 128] = ok ? sum_strided(g.lineB + gj, g.N, g.kch) : 0.0;
+                    if (MODE == MODE_FT_PRE)
+                        pre_s[q - 128] = ok ? sum_strided(g.Spre + tm * g.N + gj, g.stride_s, g.splits_s) : 0.0;
+                } else if (q == 256) {
+                    nrm_max[0] = max_strided(g.tmaxA + tm, ntm, g.kch);
+                } else {
+                    nrm_max[1] = max_strided(g.tmaxB + tn, ntn, g.kch);
+                }
             }
             mbar_arrive(&norm_bar);
         }
-        if (ALL_TMA && pt != 0) return;
-        for (int kt = STAGES; kt < ktiles; kt++) {
-            mbar_wait(&empty_bar[kt % STAGES], ((kt / STAGES) - 1) & 1);
-            produce(kt);
+        if (ALL_TMA) {
+            if (pt != 0) return;
+            for (int kt = 0; kt < ktiles; kt++) {
+                if (kt >= STAGES) mbar_wait(&empty_bar[kt % STAGES], ((kt / STAGES) - 1) & 1);
+                produce(kt);
+            }
+        } else {
+            for (int kt = 0; kt < ktiles; kt++) {
+                if (kt >= STAGES) mbar_wait(&empty_bar[kt % STAGES], ((kt / STAGES) - 1) & 1);
+                produce(kt);
+            }
+            cp_wait<0>();
         }
-        if (!ALL_TMA) cp_wait<0>();
         return;
     }
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(MMA_REGS));
@@ -649,49 +680,85 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     auto col_of = [&](int b, int e) { return frag_mn<KCB>(wn * WN, b, 2 * (lane & 3) + e); };
 
     const bool beta0 = (g.beta == 0.0);
+    // The epilogue stages the C tile in smem ([128 cols][LDT], reusing the drained pipeline):
+    // C0 arrives with cp.async (every load of the tile in flight at once, zero-fill outside
+    // M x N), out = alpha acc + beta C0 is formed per fragment element, and the tile leaves
+    // with coalesced column stores.
+    double *tileS = smem;
+    const long long mvalid = min((long long)BM, g.M - m0), nvalid = min((long long)BN, g.N - n0);
+    auto stage_c0 = [&]() {
+        if (g.vecC) {
+#pragma unroll 8
+            for (int idx = tid; idx < BM * BN / 2; idx += NTHREADS) {
+                const int row = (idx & 63) * 2, col = idx >> 6;
+                const long long gi = m0 + row, gj = n0 + col;
+                const int nv = (gj < g.N) ? (int)min(2ll, max(0ll, g.M - gi)) : 0;
+                cp_async16(tileS + row + col * LDT, nv ? g.C + gi + gj * g.ldc : g.C, nv * 8);
+            }
+        } else {
+#pragma unroll 8
+            for (int idx = tid; idx < BM * BN; idx += NTHREADS) {
+                const int row = idx & 127, col = idx >> 7;
+                const long long gi = m0 + row, gj = n0 + col;
+                const bool ok = gi < g.M && gj < g.N;
+                cp_async8(tileS + row + col * LDT, ok ? g.C + gi + gj * g.ldc : g.C, ok ? 8 : 0);
+            }
+        }
+        cp_commit();
+        cp_wait<0>();
+    };
+    // out = alpha acc + beta c0 -> smem tile (each element read/written by its owner thread)
+    auto form_out = [&]() {
+#pragma unroll
+        for (int a = 0; a < FM; a++)
+#pragma unroll
+            for (int b = 0; b < FN; b++)
+#pragma unroll
+                for (int e = 0; e < 2; e++) {
+                    const int row = row_of(a), col = col_of(b, e);
+                    const bool ok = row < mvalid && col < nvalid;
+                    double o;
+                    if (beta0) o = g.alpha * acc[a][b][e];
+                    else       o = fma(g.alpha, acc[a][b][e], g.beta * tileS[row + col * LDT]);
+                    tileS[row + col * LDT] = ok ? o : 0.0;
+                }
+    };
+    auto store_tile = [&]() {
+        if (g.vecC) {
+#pragma unroll 8
+            for (int idx = tid; idx < BM * BN / 2; idx += NTHREADS) {
+                const int row = (idx & 63) * 2, col = idx >> 6;
+                if (col >= nvalid || row >= mvalid) continue;
+                double *dst = g.C + (m0 + row) + (n0 + col) * g.ldc;
+                if (row + 1 < mvalid) *reinterpret_cast<double2 *>(dst) = *reinterpret_cast<const double2 *>(tileS + row + col * LDT);
+                else                  *dst = tileS[row + col * LDT];
+            }
+        } else {
+            for (int idx = tid; idx < BM * BN; idx += NTHREADS) {
+                const int row = idx & 127, col = idx >> 7;
+                if (row < mvalid && col < nvalid) g.C[(m0 + row) + (n0 + col) * g.ldc] = tileS[row + col * LDT];
+            }
+        }
+    };
+
     if (!FT) {
         // ---------------------------------------------------------- non-FT epilogue
-        // Straight from the accumulator fragments: for fixed (a, b, e) a warp writes 4 columns
-        // x 8 rows (full 32-byte sectors).  C0 is software-pipelined by fragment row-group: the
-        // loads of group a+1 are issued before the stores of group a (different addresses), so
-        // two groups of independent loads are in flight.
-        auto load_c0 = [&](int a, double (&c0)[FN][2]) {
-            const long long gi = m0 + row_of(a);
-#pragma unroll
-            for (int b = 0; b < FN; b++)
-#pragma unroll
-                for (int e = 0; e < 2; e++) {
-                    const long long gj = n0 + col_of(b, e);
-                    c0[b][e] = (!beta0 && gi < g.M && gj < g.N) ? __ldcs(g.C + gi + gj * g.ldc) : 0.0;
-                }
-        };
-        double c0[2][FN][2];
-        load_c0(0, c0[0]);
-#pragma unroll
-        for (int a = 0; a < FM; a++) {
-            if (a + 1 < FM) load_c0(a + 1, c0[(a + 1) & 1]);
-            const long long gi = m0 + row_of(a);
-#pragma unroll
-            for (int b = 0; b < FN; b++)
-#pragma unroll
-                for (int e = 0; e < 2; e++) {
-                    const long long gj = n0 + col_of(b, e);
-                    if (gi < g.M && gj < g.N)
-                        g.C[gi + gj * g.ldc] =
-                            beta0 ? g.alpha * acc[a][b][e] : fma(g.alpha, acc[a][b][e], g.beta * c0[a & 1][b][e]);
-                }
+        if (!beta0) {
+            stage_c0();
+            bar_mma();
         }
+        form_out();
+        bar_mma();
+        store_tile();
         return;
     }
 
     // -------------------------------------------------------------- FT epilogue
-    double *tileS = smem;                    // [128 cols][LDT]
     double *rowS = tileS + 128 * LDT;        // [2][128]
     double *rowC = rowS + 256, *rowCA = rowC + 256;
     double *colS = rowCA + 256, *colC = colS + 128, *colCA = colC + 128;
     double *rsp = colCA + 128, *ssp = rsp + 256, *dres = ssp + 256;
     int *flags = reinterpret_cast<int *>(dres + 128);  // [0] nrow, [1] ncol, [2..129] rows, [130..257] cols
-    const long long mvalid = min((long long)BM, g.M - m0), nvalid = min((long long)BN, g.N - n0);
 
     // checksum reference: FUSED -- combine the 4 k-lanes of the mainloop partials (fixed order),
     // one writer per row / column; FT_PRE -- the checksum-GEMM slices staged by the producer
@@ -718,27 +785,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // C0 tile -> smem, then its row/column sums (the beta C encoding)
     const int rr = tid & 127, hh = tid >> 7;
     if (!beta0) {
-        // C0 tile -> smem with cp.async: every load of the tile is in flight at once
-        // (zero-fill outside M x N)
-        if (g.vecC) {
-#pragma unroll 8
-            for (int idx = tid; idx < BM * BN / 2; idx += NTHREADS) {
-                const int row = (idx & 63) * 2, col = idx >> 6;
-                const long long gi = m0 + row, gj = n0 + col;
-                const int nv = (gj < g.N) ? (int)min(2ll, max(0ll, g.M - gi)) : 0;
-                cp_async16(tileS + row + col * LDT, nv ? g.C + gi + gj * g.ldc : g.C, nv * 8);
-            }
-        } else {
-#pragma unroll 8
-            for (int idx = tid; idx < BM * BN; idx += NTHREADS) {
-                const int row = idx & 127, col = idx >> 7;
-                const long long gi = m0 + row, gj = n0 + col;
-                const bool ok = gi < g.M && gj < g.N;
-                cp_async8(tileS + row + col * LDT, ok ? g.C + gi + gj * g.ldc : g.C, ok ? 8 : 0);
-            }
-        }
-        cp_commit();
-        cp_wait<0>();
+        stage_c0();
         bar_mma();
         double s = 0.0, sa = 0.0;
         for (int c = hh * 64; c < hh * 64 + 64; c++) {
@@ -780,20 +827,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     }
         }
     }
-    // out = alpha acc + beta c0 -> smem tile (each element read/written by its owner thread)
-#pragma unroll
-    for (int a = 0; a < FM; a++)
-#pragma unroll
-        for (int b = 0; b < FN; b++)
-#pragma unroll
-            for (int e = 0; e < 2; e++) {
-                const int row = row_of(a), col = col_of(b, e);
-                const bool ok = row < mvalid && col < nvalid;
-                double o;
-                if (beta0) o = g.alpha * acc[a][b][e];
-                else       o = fma(g.alpha, acc[a][b][e], g.beta * tileS[row + col * LDT]);
-                tileS[row + col * LDT] = ok ? o : 0.0;
-            }
+    form_out();
     bar_mma();
     // row / column sums of the computed tile (warp-shuffle reductions for the columns)
     {
@@ -893,10 +927,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         bar_mma();
     }
     // coalesced store of the verified tile
-    for (int idx = tid; idx < BM * BN; idx += NTHREADS) {
-        const int row = idx & 127, col = idx >> 7;
-        if (row < mvalid && col < nvalid) g.C[(m0 + row) + (n0 + col) * g.ldc] = tileS[row + col * LDT];
-    }
+    store_tile();
 }
 
 
@@ -1004,7 +1035,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int b = 0; b < FQ; b++)
 #pragma unroll
             for (int e = 0; e < 2; e++) {
-                const long long q = 8 * b + 2 * (lane & 3) + e;
+                const long long q = frag_mn<true>(0, b, 2 * (lane & 3) + e);
                 if (pi < g.P && q < g.Q) out[pi + q * g.ldo] = acc[a][b][e];
             }
     }

@@ -92,3 +92,16 @@ def test_product_has_no_oracle_or_cpu_fallback():
                 assert "import oracle" not in s and "from oracle" not in s, f
                 assert "ftblas_oracle" not in s, f
                 assert "numpy.matmul" not in s and "np.matmul" not in s and " @ " not in s, f
+
+
+def test_checksum_mode_api(lib):
+    """ftblas_set_checksum_mode accepts the two modes of the header and rejects others
+    (host-side state only, no GPU)."""
+    assert lib.ftblas_get_checksum_mode() == lib.CHECKSUM_GEMM  # default
+    lib.ftblas_set_checksum_mode("fused")
+    assert lib.ftblas_get_checksum_mode() == lib.CHECKSUM_FUSED
+    with pytest.raises(lib.FtblasError):
+        lib.ftblas_set_checksum_mode(7)
+    assert lib.ftblas_get_checksum_mode() == lib.CHECKSUM_FUSED
+    lib.ftblas_set_checksum_mode("gemm")
+    assert lib.ftblas_get_checksum_mode() == lib.CHECKSUM_GEMM
