@@ -440,7 +440,10 @@ template <int MODE>
 struct SmemPlan {
     static constexpr int STAGE_EL = 2 * TILE_EL;
     static constexpr int PIPE_EL = STAGES * STAGE_EL + (MODE == MODE_FT_FUSED ? STAGES * 2 * BK : 0);
-    static constexpr int EL = (MODE != MODE_NOFT && EPI_EL > PIPE_EL) ? EPI_EL : PIPE_EL;
+    // every mode stages the C tile ([128][LDT]) in the drained pipeline bytes; FT adds the
+    // reduction arrays
+    static constexpr int EPI = MODE != MODE_NOFT ? EPI_EL : 128 * LDT;
+    static constexpr int EL = EPI > PIPE_EL ? EPI : PIPE_EL;
     static constexpr int BYTES = 8 * EL + 1024;  // + alignment slack
 };
 
