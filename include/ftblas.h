@@ -90,6 +90,22 @@ int ftblas_dgemm(char transA, char transB, int64_t M, int64_t N, int64_t K, doub
                  const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
                  double *C, int64_t ldc, ftblas_err_report *err_report);
 
+/* ftblas_dgemm on a block of a larger problem (sharded / chunked callers).  The call's C
+ * is the block of the caller's C starting at (row_offset, col_offset), both >= 0 and
+ * multiples of FTBLAS_TILE_M / FTBLAS_TILE_N (else -14 / -15).  Report entries (i, j,
+ * tile_m, tile_n) are given in the caller's coordinates, and the fault plan of
+ * ftblas_set_fault_plan is read in the caller's coordinates (entries outside the block are
+ * ignored).  flags: FTBLAS_REPORT_APPEND -- append to the device report instead of resetting
+ * it (clear it with ftblas_report_reset); other bits -> -16. */
+#define FTBLAS_REPORT_APPEND 1
+int ftblas_dgemm_ex(char transA, char transB, int64_t M, int64_t N, int64_t K, double alpha,
+                    const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
+                    double *C, int64_t ldc, int64_t row_offset, int64_t col_offset, int32_t flags,
+                    ftblas_err_report *err_report);
+
+/* Clear the device report (stream-ordered; for FTBLAS_REPORT_APPEND sequences). */
+int ftblas_report_reset(void);
+
 /* The same DGEMM without fault tolerance (same tiles and mainloop, no checksums,
  * no verification, no injection): the baseline for the FT overhead. */
 int ftblas_dgemm_noft(char transA, char transB, int64_t M, int64_t N, int64_t K, double alpha,

@@ -44,7 +44,7 @@ struct Ctx {
     long long rep_cap = 1 << 16;
     DevBuf plan_dev;      // fault plan arrays
     DevBuf plan_ptr_dev;  // CSR offsets for the last (M,N) shape
-    long long plan_ptr_M = -1, plan_ptr_N = -1, plan_version = 0, plan_uploaded = -1;
+    long long plan_ptr_M = -1, plan_ptr_N = -1, plan_version = 0, plan_uploaded = -1, plan_off_i = 0, plan_off_j = 0;
     long long plan_n_dev = 0;
     std::vector<long long> plan_i, plan_j;
     std::vector<int> plan_bit;
@@ -162,13 +162,15 @@ bool vec_ok(const void *p, long long ld) {
     return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && (ld % 2 == 0);
 }
 
-// Upload the CSR (by tile, tile index tn*ntm + tm) of the fault plan restricted to M x N.
-int prepare_plan(long long M, long long N, GemmArgs &g) {
+// Upload the CSR (by tile, tile index tn*ntm + tm) of the fault plan restricted to the call's
+// block [off_i, off_i + M) x [off_j, off_j + N) of the caller's C, in call-relative indices.
+int prepare_plan(long long M, long long N, long long off_i, long long off_j, GemmArgs &g) {
     Ctx &c = ctx();
     g.plan_ptr = nullptr; g.plan_i = nullptr; g.plan_j = nullptr; g.plan_bit = nullptr;
     if (c.plan_i.empty()) return 0;
     const size_t bytes_ij0 = std::max<size_t>(1, c.plan_i.size()) * sizeof(long long);
-    if (c.plan_uploaded == c.plan_version && c.plan_ptr_M == M && c.plan_ptr_N == N) {  // cached upload
+    if (c.plan_uploaded == c.plan_version && c.plan_ptr_M == M && c.plan_ptr_N == N && c.plan_off_i == off_i &&
+        c.plan_off_j == off_j) {  // cached upload
         char *base = c.plan_dev.as<char>();
         g.plan_ptr = c.plan_ptr_dev.as<int>();
         g.plan_i = reinterpret_cast<const long long *>(base);
@@ -180,7 +182,7 @@ int prepare_plan(long long M, long long N, GemmArgs &g) {
     std::vector<int> cnt(nt + 1, 0);
     std::vector<long long> order;
     for (size_t f = 0; f < c.plan_i.size(); f++) {
-        const long long i = c.plan_i[f], j = c.plan_j[f];
+        const long long i = c.plan_i[f] - off_i, j = c.plan_j[f] - off_j;
         if (i < 0 || i >= M || j < 0 || j >= N) continue;
         cnt[(j / BN) * ntm + i / BM + 1]++;
         order.push_back((long long)f);
@@ -191,7 +193,7 @@ int prepare_plan(long long M, long long N, GemmArgs &g) {
     std::vector<long long> pi(n), pj(n);
     std::vector<int> pb(n);
     for (long long f : order) {
-        const long long i = c.plan_i[f], j = c.plan_j[f];
+        const long long i = c.plan_i[f] - off_i, j = c.plan_j[f] - off_j;
         const int pos = fill[(j / BN) * ntm + i / BM]++;
         pi[pos] = i; pj[pos] = j; pb[pos] = c.plan_bit[f];
     }
@@ -206,7 +208,7 @@ int prepare_plan(long long M, long long N, GemmArgs &g) {
     CK(cudaMemcpyAsync(base + 2 * bytes_ij, pb.data(), n * sizeof(int), cudaMemcpyHostToDevice, c.stream), "plan bit");
     CK(cudaMemcpyAsync(c.plan_ptr_dev.p, cnt.data(), (nt + 1) * sizeof(int), cudaMemcpyHostToDevice, c.stream), "plan ptr");
     CK(cudaStreamSynchronize(c.stream), "plan upload");
-    c.plan_uploaded = c.plan_version; c.plan_ptr_M = M; c.plan_ptr_N = N;
+    c.plan_uploaded = c.plan_version; c.plan_ptr_M = M; c.plan_ptr_N = N; c.plan_off_i = off_i; c.plan_off_j = off_j;
     g.plan_ptr = c.plan_ptr_dev.as<int>();
     g.plan_i = reinterpret_cast<const long long *>(base);
     g.plan_j = reinterpret_cast<const long long *>(base + bytes_ij);
@@ -319,7 +321,8 @@ cudaError_t cksum_gemm(bool kcx, const double *X, long long ldx, long long P, co
 
 int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K, double alpha,
                const double *A, long long lda, const double *B, long long ldb, double beta, double *C,
-               long long ldc, ftblas_err_report *rep) {
+               long long ldc, ftblas_err_report *rep, long long off_i = 0, long long off_j = 0,
+               bool append = false) {
     static_assert(sizeof(Correction) == sizeof(ftblas_correction), "ABI");
     Ctx &c = ctx();
     int rc = check_args(ta, tb, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta);
@@ -328,7 +331,7 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
         CK(c.rep.ensure(sizeof(ReportHdr) + c.rep_cap * sizeof(Correction)), "cudaMalloc(report)");
     }
     if (M == 0 || N == 0) {
-        if (ft) CK(cudaMemsetAsync(c.rep.p, 0, sizeof(ReportHdr), c.stream), "report reset");
+        if (ft && !append) CK(cudaMemsetAsync(c.rep.p, 0, sizeof(ReportHdr), c.stream), "report reset");
         return rep ? fetch_report(rep) : 0;
     }
     const bool kca = is_t(ta), kcb = !is_t(tb);
@@ -376,13 +379,14 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
         g.rep_entries = reinterpret_cast<Correction *>(c.rep.as<char>() + sizeof(ReportHdr));
         g.rep_cap = c.rep_cap;
         g.vecC = vec_ok(C, ldc) ? 1 : 0;
-        rc = prepare_plan(M, N, g);
+        g.off_i = off_i; g.off_j = off_j;
+        rc = prepare_plan(M, N, off_i, off_j, g);
         if (rc) return rc;
         EncodeArgs ea{};
         ea.op[0] = EncodeOperand{A, lda, M, kca ? 1 : 0, va ? 1 : 0, const_cast<double *>(g.VA), lineA, tmaxA, (int)ntm};
         ea.op[1] = EncodeOperand{B, ldb, N, kcb ? 1 : 0, vb ? 1 : 0, const_cast<double *>(g.WB), lineB, tmaxB, (int)ntn};
         ea.K = (alpha == 0.0) ? 0 : K;  // alpha == 0: A, B are not read (encodes are zero)
-        ea.Kp = Kp; ea.kper = kper; ea.kch = kch; ea.rep = g.rep;
+        ea.Kp = Kp; ea.kper = kper; ea.kch = kch; ea.rep = append ? nullptr : g.rep;
         dim3 grid((unsigned)std::max(ntm, ntn), (unsigned)kch, 2);
         encode_kernel<<<grid, NTHREADS, 0, c.stream>>>(ea);
         c.launches++;
@@ -426,6 +430,23 @@ int ftblas_dgemm(char transA, char transB, int64_t M, int64_t N, int64_t K, doub
                  int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,
                  ftblas_err_report *err_report) {
     return dgemm_impl(true, transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, err_report);
+}
+
+int ftblas_dgemm_ex(char transA, char transB, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
+                    int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,
+                    int64_t row_offset, int64_t col_offset, int32_t flags, ftblas_err_report *err_report) {
+    if (row_offset < 0 || row_offset % FTBLAS_TILE_M) return arg_fail(14, "row_offset not a multiple of the tile");
+    if (col_offset < 0 || col_offset % FTBLAS_TILE_N) return arg_fail(15, "col_offset not a multiple of the tile");
+    if (flags & ~FTBLAS_REPORT_APPEND) return arg_fail(16, "unknown flags");
+    return dgemm_impl(true, transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, err_report, row_offset,
+                      col_offset, (flags & FTBLAS_REPORT_APPEND) != 0);
+}
+
+int ftblas_report_reset(void) {
+    Ctx &c = ctx();
+    CK(c.rep.ensure(sizeof(ReportHdr) + c.rep_cap * sizeof(Correction)), "cudaMalloc(report)");
+    CK(cudaMemsetAsync(c.rep.p, 0, sizeof(ReportHdr), c.stream), "report reset");
+    return 0;
 }
 
 int ftblas_dgemm_noft(char transA, char transB, int64_t M, int64_t N, int64_t K, double alpha, const double *A,

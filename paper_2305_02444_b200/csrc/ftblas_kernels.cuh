@@ -141,6 +141,7 @@ struct GemmArgs {
     ReportHdr *rep;
     Correction *rep_entries;
     long long rep_cap;
+    long long off_i, off_j;  // position of this call's C block in the caller's C (report indices)
     int vecC;              // C 16-byte aligned with even ldc (cp.async16 staging of C0)
 };
 
@@ -920,7 +921,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 const unsigned long long p = atomicAdd(&g.rep->count, 1ull);
                 if ((long long)p < g.rep_cap) {
                     Correction cr;
-                    cr.tile_m = tm; cr.tile_n = tn; cr.i = gi; cr.j = gj;
+                    cr.tile_m = tm + g.off_i / BM; cr.tile_n = tn + g.off_j / BN;
+                    cr.i = gi + g.off_i; cr.j = gj + g.off_j;
                     cr.residual = dres[r];
                     cr.kind = single ? 1 : 2; cr.pad = 0;
                     g.rep_entries[p] = cr;

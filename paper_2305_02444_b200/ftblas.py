@@ -66,6 +66,10 @@ def _load():
     L.ftblas_last_error.restype = ct.c_char_p
     L.ftblas_release.argtypes = []
     L.ftblas_release.restype = ct.c_int
+    L.ftblas_dgemm_ex.argtypes = common + [I, I, ct.c_int32, ct.POINTER(ftblas_err_report)]
+    L.ftblas_dgemm_ex.restype = ct.c_int
+    L.ftblas_report_reset.argtypes = []
+    L.ftblas_report_reset.restype = ct.c_int
     L.ftblas_set_checksum_mode.argtypes = [ct.c_int]
     L.ftblas_set_checksum_mode.restype = ct.c_int
     L.ftblas_get_checksum_mode.argtypes = []
@@ -79,7 +83,10 @@ lib = _load()
 EXPORTS = ("ftblas_dgemm", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_report_fetch",
            "ftblas_set_fault_plan", "ftblas_set_stream", "ftblas_launch_count",
            "ftblas_tile_shape", "ftblas_last_error", "ftblas_release", "ftblas_profile",
-           "ftblas_profile_read", "ftblas_set_checksum_mode", "ftblas_get_checksum_mode")
+           "ftblas_profile_read", "ftblas_set_checksum_mode", "ftblas_get_checksum_mode",
+           "ftblas_dgemm_ex", "ftblas_report_reset")
+
+REPORT_APPEND = 1  # FTBLAS_REPORT_APPEND
 
 CHECKSUM_GEMM = 0   # FTBLAS_CHECKSUM_GEMM: checksum row/column by two DMMA GEMMs (default)
 CHECKSUM_FUSED = 1  # FTBLAS_CHECKSUM_FUSED: accumulated in the main GEMM's mainloop
@@ -144,6 +151,19 @@ def ftblas_dgemm(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, r
     _check(lib.ftblas_dgemm(_tc(transA), _tc(transB), M, N, K, alpha, _ptr(A), lda, _ptr(B), ldb,
                             beta, _ptr(C), ldc, rep))
     return report
+
+
+def ftblas_dgemm_ex(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, row_offset=0,
+                    col_offset=0, append=False, report=None):
+    rep = ct.byref(report.c) if report is not None else None
+    _check(lib.ftblas_dgemm_ex(_tc(transA), _tc(transB), M, N, K, alpha, _ptr(A), lda, _ptr(B), ldb,
+                               beta, _ptr(C), ldc, row_offset, col_offset,
+                               REPORT_APPEND if append else 0, rep))
+    return report
+
+
+def ftblas_report_reset():
+    _check(lib.ftblas_report_reset())
 
 
 def ftblas_dgemm_noft(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc):

@@ -18,6 +18,7 @@ from dataclasses import dataclass
 import numpy as np
 
 TILE_M = 128
+TILE_N = 128
 
 
 def shard_rows(M: int, world: int, rank: int, align: int = TILE_M) -> tuple:
@@ -55,21 +56,58 @@ def broadcast_b(B, src: int = 0, group=None):
     return B
 
 
+def chunk_bounds(N: int, chunks: int, align: int = TILE_N) -> list:
+    """Column blocks [c0, c1) of whole verification tiles covering [0, N), as even as possible."""
+    tiles = -(-N // align)
+    chunks = max(1, min(chunks, tiles))
+    per, rem = divmod(tiles, chunks)
+    out, t0 = [], 0
+    for c in range(chunks):
+        t1 = t0 + per + (1 if c < rem else 0)
+        out.append((min(N, t0 * align), min(N, t1 * align)))
+        t0 = t1
+    return out
+
+
 def sharded_dgemm(gemm, transA, transB, M, N, K, alpha, A_shard, lda, B, ldb, beta, C_shard, ldc,
                   *, rank: int, world: int, src: int = 0, group=None, broadcast: bool = True,
-                  report=None):
+                  chunks: int = 1):
     """One sharded step on this rank.
 
-    ``gemm(transA, transB, m, N, K, alpha, A, lda, B, ldb, beta, C, ldc, report)`` is the
-    single-device call (``ftblas.ftblas_dgemm`` in production).  A_shard holds this rank's
-    rows of op(A) (for transA='N' an (r1-r0) x K block, lda >= r1-r0; for 'T' a K x (r1-r0)
-    block), C_shard its (r1-r0) x N rows of C.  Returns the local rows range.
+    ``gemm(transA, transB, m, n, K, alpha, A, lda, B, ldb, beta, C, ldc, col_offset, append)``
+    is the single-device call on the column block [col_offset, col_offset + n) of this rank's
+    C (``ftblas.ftblas_dgemm_ex`` in production: reports in block-global column coordinates,
+    ``append`` keeps the device report of the earlier blocks).  A_shard holds this rank's rows
+    of op(A) (for transA='N' an (r1-r0) x K block, lda >= r1-r0; for 'T' a K x (r1-r0) block),
+    C_shard its (r1-r0) x N rows of C as flat column-major storage (ld ``ldc``), B the flat
+    column-major storage of B (ld ``ldb``).
+
+    The exchange of the step is the broadcast of op(B) from ``src``.  With ``chunks > 1`` and
+    transB = 'N' (column blocks of op(B) are contiguous in B) it is split into column blocks
+    of whole tiles, all posted asynchronously on the communication stream; the GEMM of block
+    c waits only for block c, so the broadcast of the later blocks overlaps the DMMA work of
+    the earlier ones.  Returns this rank's rows range.
     """
     r0, r1 = shard_rows(M, world, rank)
-    if broadcast:
-        broadcast_b(B, src, group)
     m = r1 - r0
-    gemm(transA, transB, m, N, K, alpha, A_shard, lda, B, ldb, beta, C_shard, ldc, report)
+    multi = broadcast and world > 1
+    if multi and chunks > 1 and transB in ("N", "n"):
+        import torch.distributed as dist
+        bounds = chunk_bounds(N, chunks)
+        works = [dist.broadcast(B[c0 * ldb: c1 * ldb], src=src, group=group, async_op=True)
+                 for (c0, c1) in bounds]
+        for q, (c0, c1) in enumerate(bounds):
+            if rank != src:
+                works[q].wait()  # NCCL: the compute stream waits for block q, the host does not
+            gemm(transA, transB, m, c1 - c0, K, alpha, A_shard, lda, B[c0 * ldb:], ldb, beta,
+                 C_shard[c0 * ldc:], ldc, c0, q > 0)
+        if rank == src:
+            for w in works:
+                w.wait()
+        return r0, r1
+    if multi:
+        broadcast_b(B, src, group)
+    gemm(transA, transB, m, N, K, alpha, A_shard, lda, B, ldb, beta, C_shard, ldc, 0, False)
     return r0, r1
 
 

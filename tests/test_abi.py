@@ -105,3 +105,13 @@ def test_checksum_mode_api(lib):
     assert lib.ftblas_get_checksum_mode() == lib.CHECKSUM_FUSED
     lib.ftblas_set_checksum_mode("gemm")
     assert lib.ftblas_get_checksum_mode() == lib.CHECKSUM_GEMM
+
+
+@pytest.mark.parametrize("roff,coff,flags,code", [(64, 0, 0, -14), (-128, 0, 0, -14), (0, 5, 0, -15),
+                                                  (0, 0, 2, -16)])
+def test_ex_argument_errors(lib, roff, coff, flags, code):
+    """ftblas_dgemm_ex rejects offsets that are not whole tiles and unknown flags before any
+    CUDA call (so this runs without a GPU)."""
+    rc = lib.lib.ftblas_dgemm_ex(b"N", b"N", 4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, roff, coff,
+                                 flags, None)
+    assert rc == code

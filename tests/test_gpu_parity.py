@@ -211,6 +211,42 @@ def test_host_buffer_entry_point(ft):
     assert_close(w, d, C, C_ref)
 
 
+@pytest.mark.parametrize("split", ["cols", "rows"])
+def test_blocked_calls_with_offsets_and_append(ft, split):
+    """ftblas_dgemm_ex on column blocks (the chunked broadcast path) or row blocks (shards)
+    with a global fault plan and FTBLAS_REPORT_APPEND: the accumulated report must equal
+    the oracle's report of the whole problem, and C must match."""
+    import torch
+    w = syn.Workload("blk", 400, 520, 70, "N", "N", 1.25, 0.5, "uniform", True, seed=23)
+    d = syn.make_inputs(w)
+    plan = syn.fault_plan(w.M, w.N, 6, 9)
+    A_t, pA = to_dev(d["A"]); B_t, pB = to_dev(d["B"]); C_t, pC = to_dev(d["C"])
+    ft.ftblas_set_fault_plan(*plan)
+    ft.ftblas_report_reset()
+    if split == "cols":
+        for q, (c0, c1) in enumerate([(0, 256), (256, 384), (384, 520)]):
+            ft.ftblas_dgemm_ex("N", "N", w.M, c1 - c0, w.K, w.alpha, pA, d["lda"], pB + 8 * c0 * d["ldb"],
+                               d["ldb"], w.beta, pC + 8 * c0 * d["ldc"], d["ldc"], 0, c0, q > 0)
+    else:
+        for q, (r0, r1) in enumerate([(0, 128), (128, 400)]):
+            ft.ftblas_dgemm_ex("N", "N", r1 - r0, w.N, w.K, w.alpha, pA + 8 * r0, d["lda"], pB, d["ldb"],
+                               w.beta, pC + 8 * r0, d["ldc"], r0, 0, q > 0)
+    rep = ft.ftblas_report_fetch(ft.Report(64))
+    ft.ftblas_clear_fault_plan()
+    C = from_dev(C_t, d["C"])
+    C_ref, orep, st = run_oracle(w, d, plan)
+    assert rep.count == st.count == 6
+    assert report_key(rep.entries()) == report_key(orep)
+    assert_close(w, d, C, C_ref)
+
+
+def test_ex_argument_errors(ft):
+    with pytest.raises(ft.FtblasError):
+        ft.ftblas_dgemm_ex("N", "N", 4, 4, 4, 1.0, 0, 4, 0, 4, 0.0, 0, 4, 64, 0)
+    with pytest.raises(ft.FtblasError):
+        ft.ftblas_dgemm_ex("N", "N", 4, 4, 4, 1.0, 0, 4, 0, 4, 0.0, 0, 4, 0, 5)
+
+
 # ---------------------------------------------------------------- BASELINE configs
 def test_config0_all_flips_corrected(ftd):
     w = syn.CONFIGS[0]

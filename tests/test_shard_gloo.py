@@ -24,11 +24,11 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, tA, q):
+def _worker(rank, world, port, tA, chunks, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        w = syn.Workload("shard", 300, 140, 50, tA, "N", 1.5, -0.5, "uniform", True, seed=17)
+        w = syn.Workload("shard", 300, 300, 50, tA, "N", 1.5, -0.5, "uniform", True, seed=17)
         d = syn.make_inputs(w)
         plan = syn.fault_plan(w.M, w.N, 3, 4)
         r0, r1 = shard.shard_rows(w.M, world, rank)
@@ -42,16 +42,28 @@ def _worker(rank, world, port, tA, q):
         B_t = torch.from_numpy(np.asfortranarray(d["B"]).reshape(-1, order="F").copy()) if rank == 0 \
             else torch.zeros(d["B"].size, dtype=torch.float64)
         pl = shard.shard_plan(plan, r0, r1)
-        captured = {}
+        captured = {"entries": []}
+        C_flat = torch.from_numpy(C_loc.reshape(-1, order="F").copy())
 
-        def cpu_gemm(ta, tb, M_, N_, K_, al, A_, lda_, B_, ldb_, be, C_, ldc_, rep):
-            Bm = B_.numpy().reshape((ldb_, -1), order="F")
-            entries, st = oracle.abft_dgemm(ta, tb, M_, N_, K_, al, A_, lda_, Bm, ldb_, be, C_, ldc_,
-                                            faults=pl)
-            captured["entries"] = entries
+        def cpu_gemm(ta, tb, M_, N_, K_, al, A_, lda_, B_, ldb_, be, C_, ldc_, col_offset, append):
+            # the oracle on the column block [col_offset, col_offset + N_) of this rank's C
+            Bm = B_.numpy()[: ldb_ * N_].reshape((ldb_, N_), order="F")
+            Cm = C_.numpy()[: ldc_ * N_].reshape((ldc_, N_), order="F")
+            plj = None
+            if pl is not None:
+                sel = (pl[1] >= col_offset) & (pl[1] < col_offset + N_)
+                plj = (pl[0][sel], pl[1][sel] - col_offset, pl[2][sel])
+            entries, st = oracle.abft_dgemm(ta, tb, M_, N_, K_, al, A_, lda_, Bm, ldb_, be, Cm, ldc_,
+                                            faults=plj)
+            for e in entries:  # block-global columns, as ftblas_dgemm_ex reports them
+                e = dict(e)
+                e["j"] = int(e["j"]) + col_offset
+                e["tile_n"] = int(e["tile_n"]) + col_offset // 128
+                captured["entries"].append(e)
 
         shard.sharded_dgemm(cpu_gemm, tA, "N", w.M, w.N, w.K, w.alpha, A_loc, lda, B_t, d["ldb"],
-                            w.beta, C_loc, max(1, m), rank=rank, world=world)
+                            w.beta, C_flat, max(1, m), rank=rank, world=world, chunks=chunks)
+        C_loc = C_flat.numpy().reshape((max(1, m), w.N), order="F")[:m]
         ents = shard.gather_reports(shard.globalize(captured["entries"], r0))
         parts = [None] * world
         dist.all_gather_object(parts, (r0, r1, C_loc))
@@ -61,20 +73,20 @@ def _worker(rank, world, port, tA, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("tA", ["N", "T"])
-def test_sharded_equals_unsharded(tA):
+@pytest.mark.parametrize("tA,chunks", [("N", 1), ("T", 1), ("N", 2), ("T", 3)])
+def test_sharded_equals_unsharded(tA, chunks):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, tA, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, tA, chunks, q)) for r in range(world)]
     for p in procs:
         p.start()
     ents, parts = q.get(timeout=240)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    w = syn.Workload("shard", 300, 140, 50, tA, "N", 1.5, -0.5, "uniform", True, seed=17)
+    w = syn.Workload("shard", 300, 300, 50, tA, "N", 1.5, -0.5, "uniform", True, seed=17)
     d = syn.make_inputs(w)
     plan = syn.fault_plan(w.M, w.N, 3, 4)
     C = np.asfortranarray(d["C"].copy())
@@ -96,3 +108,14 @@ def test_shard_rows_cover_whole_tiles():
     plan = (np.array([5, 130, 260]), np.array([1, 2, 3]), np.array([40, 50, 60]))
     i, j, b = shard.shard_plan(plan, 128, 256)
     assert i.tolist() == [2] and j.tolist() == [2] and b.tolist() == [50]
+
+
+def test_chunk_bounds_whole_tiles():
+    assert shard.chunk_bounds(300, 2) == [(0, 256), (256, 300)]
+    assert shard.chunk_bounds(300, 8) == [(0, 128), (128, 256), (256, 300)]
+    for N in (1, 128, 129, 16384, 16500):
+        for ch in (1, 2, 3, 8):
+            b = shard.chunk_bounds(N, ch)
+            assert b[0][0] == 0 and b[-1][1] == N
+            assert all(c0 % 128 == 0 and c0 < c1 for c0, c1 in b)
+            assert all(p[1] == q[0] for p, q in zip(b, b[1:]))
