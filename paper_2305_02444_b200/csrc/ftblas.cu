@@ -49,6 +49,20 @@ struct Ctx {
     std::vector<long long> plan_i, plan_j;
     std::vector<int> plan_bit;
     DevBuf hA, hB, hC;    // ftblas_dgemm_host device staging
+    cudaStream_t s_up = nullptr, s_down = nullptr;  // ftblas_dgemm_host copy streams
+    cudaEvent_t ev_entry = nullptr, ev_exit = nullptr, ev_up[8] = {}, ev_done[8] = {};
+    cudaError_t ensure_copy_streams() {
+        if (s_up) return cudaSuccess;
+        cudaError_t e = cudaStreamCreateWithFlags(&s_up, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s_down, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_entry, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_exit, cudaEventDisableTiming);
+        for (int q = 0; q < 8 && e == cudaSuccess; q++) {
+            e = cudaEventCreateWithFlags(&ev_up[q], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_done[q], cudaEventDisableTiming);
+        }
+        return e;
+    }
     long long launches = 0;
     bool profiling = false;
     struct Rec { cudaEvent_t e0, e1, e2; bool ft; };
@@ -471,19 +485,52 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
     if (readAB) {
         CK(c.hA.ensure((size_t)dla * ac * 8), "cudaMalloc(A)");
         CK(c.hB.ensure((size_t)dlb * bc * 8), "cudaMalloc(B)");
-        CK(cudaMemcpy2DAsync(c.hA.p, dla * 8, A, lda * 8, ar * 8, ac, cudaMemcpyHostToDevice, c.stream), "H2D A");
-        CK(cudaMemcpy2DAsync(c.hB.p, dlb * 8, B, ldb * 8, br * 8, bc, cudaMemcpyHostToDevice, c.stream), "H2D B");
     }
     CK(c.hC.ensure((size_t)dlc * N * 8), "cudaMalloc(C)");
-    if (beta != 0.0)
-        CK(cudaMemcpy2DAsync(c.hC.p, dlc * 8, C, ldc * 8, M * 8, N, cudaMemcpyHostToDevice, c.stream), "H2D C");
-    rc = dgemm_impl(true, transA, transB, M, N, K, alpha, readAB ? c.hA.as<double>() : nullptr, readAB ? dla : std::max<long long>(1, ar),
-                    readAB ? c.hB.as<double>() : nullptr, readAB ? dlb : std::max<long long>(1, br), beta, c.hC.as<double>(), dlc,
-                    nullptr);
-    if (rc) return rc;
-    CK(cudaMemcpy2DAsync(C, ldc * 8, c.hC.p, dlc * 8, M * 8, N, cudaMemcpyDeviceToHost, c.stream), "D2H C");
+    CK(c.ensure_copy_streams(), "copy streams");
+    // Pipeline over column blocks of whole tiles: op(A) first (every block needs it), then per
+    // block the H2D of its op(B) columns (rows of B for 'T') and C0 columns on the upload
+    // stream, its ABFT GEMM on the library stream (report appended, block column offset), and
+    // the D2H of its verified C columns on the download stream -- the PCIe traffic of the
+    // later blocks overlaps the DMMA work of the earlier ones, both directions at once.
+    const long long tiles_n = (N + FTBLAS_TILE_N - 1) / FTBLAS_TILE_N;
+    const long long nblk = std::min<long long>(tiles_n, 8);
+    CK(cudaEventRecord(c.ev_entry, c.stream), "event");  // device buffers free once prior work is done
+    CK(cudaStreamWaitEvent(c.s_up, c.ev_entry, 0), "wait");
+    if (readAB)
+        CK(cudaMemcpy2DAsync(c.hA.p, dla * 8, A, lda * 8, ar * 8, ac, cudaMemcpyHostToDevice, c.s_up), "H2D A");
+    long long t0 = 0;
+    for (long long q = 0; q < nblk; q++) {
+        const long long t1 = t0 + tiles_n / nblk + (q < tiles_n % nblk ? 1 : 0);
+        const long long c0 = t0 * FTBLAS_TILE_N, c1 = std::min<long long>(N, t1 * FTBLAS_TILE_N), n = c1 - c0;
+        t0 = t1;
+        if (readAB) {
+            if (is_t(transB))  // op(B)(:, c0:c1) = rows c0..c1 of the N x K stored B
+                CK(cudaMemcpy2DAsync(c.hB.as<double>() + c0, dlb * 8, B + c0, ldb * 8, n * 8, K,
+                                     cudaMemcpyHostToDevice, c.s_up), "H2D B");
+            else
+                CK(cudaMemcpy2DAsync(c.hB.as<double>() + c0 * dlb, dlb * 8, B + c0 * ldb, ldb * 8, K * 8, n,
+                                     cudaMemcpyHostToDevice, c.s_up), "H2D B");
+        }
+        if (beta != 0.0)
+            CK(cudaMemcpy2DAsync(c.hC.as<double>() + c0 * dlc, dlc * 8, C + c0 * ldc, ldc * 8, M * 8, n,
+                                 cudaMemcpyHostToDevice, c.s_up), "H2D C");
+        CK(cudaEventRecord(c.ev_up[q], c.s_up), "event");
+        CK(cudaStreamWaitEvent(c.stream, c.ev_up[q], 0), "wait");
+        const double *dB = readAB ? (is_t(transB) ? c.hB.as<double>() + c0 : c.hB.as<double>() + c0 * dlb) : nullptr;
+        rc = dgemm_impl(true, transA, transB, M, n, K, alpha, readAB ? c.hA.as<double>() : nullptr,
+                        readAB ? dla : std::max<long long>(1, ar), dB, readAB ? dlb : std::max<long long>(1, br),
+                        beta, c.hC.as<double>() + c0 * dlc, dlc, nullptr, 0, c0, q > 0);
+        if (rc) return rc;
+        CK(cudaEventRecord(c.ev_done[q], c.stream), "event");
+        CK(cudaStreamWaitEvent(c.s_down, c.ev_done[q], 0), "wait");
+        CK(cudaMemcpy2DAsync(C + c0 * ldc, ldc * 8, c.hC.as<double>() + c0 * dlc, dlc * 8, M * 8, n,
+                             cudaMemcpyDeviceToHost, c.s_down), "D2H C");
+    }
+    CK(cudaEventRecord(c.ev_exit, c.s_down), "event");
+    CK(cudaStreamWaitEvent(c.stream, c.ev_exit, 0), "wait");  // later library work sees C on the host
+    CK(cudaStreamSynchronize(c.s_down), "sync");
     if (err_report) return fetch_report(err_report);
-    CK(cudaStreamSynchronize(c.stream), "sync");
     return 0;
 }
 

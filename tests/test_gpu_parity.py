@@ -196,8 +196,16 @@ def test_beta_zero_ignores_nan_in_C(ft):
     assert np.isfinite(C_gpu).all() and rep.count == 0
 
 
-def test_host_buffer_entry_point(ft):
-    w = syn.CONFIGS[0]
+@pytest.mark.parametrize("shape", ["c0", "blocks_nt", "blocks_ntn_ragged"])
+def test_host_buffer_entry_point(ft, shape):
+    """The e2e call on host buffers: pipelined over column blocks (H2D / GEMM / D2H overlap),
+    report accumulated over the blocks; must equal the oracle on the whole problem."""
+    if shape == "c0":
+        w = syn.CONFIGS[0]
+    elif shape == "blocks_nt":   # 9 column tiles -> 8 blocks, transposed B (2-D row-slab copies)
+        w = syn.Workload("hb", 300, 1100, 60, "N", "T", -0.75, 1.5, "uniform", True, seed=31, n_flips=7)
+    else:                        # ragged last tile, transposed A, beta = 0
+        w = syn.Workload("hb2", 130, 390, 33, "T", "N", 2.0, 0.0, "normal", True, seed=32, n_flips=3)
     d = syn.make_inputs(w)
     plan = syn.fault_plan(w.M, w.N, w.n_flips, w.seed)
     ft.ftblas_set_fault_plan(*plan)
@@ -326,3 +334,9 @@ def test_config2_rank_k_update(ftd):
 
 def test_config3_16384(ftd):
     check_full_config(ftd, syn.CONFIGS[3], oracle_tiles=6)
+
+
+def test_config4_32768x16384(ftd):
+    """configs[4] is quoted for an 8-GPU row-block shard; each shard runs the single-GPU call,
+    so the whole problem on one GPU (17 GB of operands) checks the same kernels at full size."""
+    check_full_config(ftd, syn.CONFIGS[4], oracle_tiles=4)
