@@ -354,6 +354,7 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
     g.A = A; g.B = B; g.C = C; g.lda = lda; g.ldb = ldb; g.ldc = ldc;
     g.M = M; g.N = N; g.K = K; g.alpha = alpha; g.beta = beta;
     const bool va = vec_ok(A, lda), vb = vec_ok(B, ldb);
+    g.vecC = vec_ok(C, ldc) ? 1 : 0;  // 16-byte C0 staging / stores in every mode
     const Staging stg = make_staging(A, lda, M, kca, B, ldb, N, kcb, K, alpha);
     Ctx::Rec rec{};
     if (c.profiling) {
