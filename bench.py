@@ -239,7 +239,9 @@ def main():
     flops_local = 2.0 * m * w.N * w.K
 
     def gemm_ft(ta, tb, M_, N_, K_, al, A_, lda_, B_, ldb_, be, C_, ldc_, col_offset, append):
-        fb.ftblas_dgemm_ex(ta, tb, M_, N_, K_, al, A_, lda_, B_, ldb_, be, C_, ldc_, 0, col_offset, append)
+        # blocks after the first reuse the checksum encoding of this rank's A (unchanged)
+        fb.ftblas_dgemm_ex(ta, tb, M_, N_, K_, al, A_, lda_, B_, ldb_, be, C_, ldc_, 0, col_offset, append,
+                           reuse_a=append)
 
     def gemm_noft(ta, tb, M_, N_, K_, al, A_, lda_, B_, ldb_, be, C_, ldc_, col_offset, append):
         fb.ftblas_dgemm_noft(ta, tb, M_, N_, K_, al, A_, lda_, B_, ldb_, be, C_, ldc_)

@@ -96,8 +96,12 @@ int ftblas_dgemm(char transA, char transB, int64_t M, int64_t N, int64_t K, doub
  * tile_m, tile_n) are given in the caller's coordinates, and the fault plan of
  * ftblas_set_fault_plan is read in the caller's coordinates (entries outside the block are
  * ignored).  flags: FTBLAS_REPORT_APPEND -- append to the device report instead of resetting
- * it (clear it with ftblas_report_reset); other bits -> -16. */
+ * it (clear it with ftblas_report_reset); FTBLAS_REUSE_A_ENCODE -- the caller guarantees that
+ * op(A) (same pointer, lda, M, K, transA) is unchanged since the previous FT call, whose A
+ * checksum encoding is then reused if still cached (column blocks of one product); other
+ * bits -> -16. */
 #define FTBLAS_REPORT_APPEND 1
+#define FTBLAS_REUSE_A_ENCODE 2
 int ftblas_dgemm_ex(char transA, char transB, int64_t M, int64_t N, int64_t K, double alpha,
                     const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
                     double *C, int64_t ldc, int64_t row_offset, int64_t col_offset, int32_t flags,

@@ -50,11 +50,27 @@ struct Ctx {
     std::vector<int> plan_bit;
     DevBuf hA, hB, hC;    // ftblas_dgemm_host device staging
     cudaStream_t s_up = nullptr, s_down = nullptr;  // ftblas_dgemm_host copy streams
+    cudaStream_t s_side = nullptr;                   // checksum GEMM S^T (forked / joined)
     cudaEvent_t ev_entry = nullptr, ev_exit = nullptr, ev_up[8] = {}, ev_done[8] = {};
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // cached A-side encoding (FTBLAS_REUSE_A_ENCODE)
+    struct AKey {
+        const void *A; long long lda, M, K; bool kc, a0;
+        bool operator==(const AKey &o) const {
+            return A == o.A && lda == o.lda && M == o.M && K == o.K && kc == o.kc && a0 == o.a0;
+        }
+    };
+    AKey a_key{};
+    bool a_valid = false;
+    int a_kch = 1;
+    long long ws_gen = 0, a_ws_gen = -1;
     cudaError_t ensure_copy_streams() {
         if (s_up) return cudaSuccess;
         cudaError_t e = cudaStreamCreateWithFlags(&s_up, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s_down, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s_side, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_entry, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_exit, cudaEventDisableTiming);
         for (int q = 0; q < 8 && e == cudaSuccess; q++) {
@@ -336,7 +352,7 @@ cudaError_t cksum_gemm(bool kcx, const double *X, long long ldx, long long P, co
 int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K, double alpha,
                const double *A, long long lda, const double *B, long long ldb, double beta, double *C,
                long long ldc, ftblas_err_report *rep, long long off_i = 0, long long off_j = 0,
-               bool append = false) {
+               bool append = false, bool reuse_a = false) {
     static_assert(sizeof(Correction) == sizeof(ftblas_correction), "ABI");
     Ctx &c = ctx();
     int rc = check_args(ta, tb, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta);
@@ -369,23 +385,38 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
         long long kch_l = (8 * 2 * 148 + ntm + ntn - 1) / (ntm + ntn);
         kch_l = std::min<long long>({kch_l, 32, std::max<long long>(1, Kp / 128)});
         int kch = (int)std::max<long long>(1, kch_l);
+        // FTBLAS_REUSE_A_ENCODE: the caller promises op(A) is unchanged since the previous call
+        // on the same A (the blocks of a chunked call); its encoding is reused when the cached
+        // key matches and the workspace was not reallocated, else A is encoded as usual.
+        const Ctx::AKey akey{A, lda, M, K, kca, alpha == 0.0};
+        const bool skip_a = reuse_a && c.a_valid && c.a_key == akey && c.a_ws_gen == c.ws_gen;
+        if (skip_a) kch = c.a_kch;
         const long long kper = ((Kp + kch - 1) / kch + 31) / 32 * 32;
-        const size_t nV = (size_t)(ntm + ntn) * Kp, nLine = (size_t)kch * (M + N), nT = (size_t)kch * (ntm + ntn);
         const bool pre = c.checksum_mode == FTBLAS_CHECKSUM_GEMM;
         long long spR = 1, kpR = Kp, spS = 1, kpS = Kp;
         if (pre) {
             cksum_split(ntm * ((ntn + 127) / 128), K, spR, kpR);
             cksum_split(ntn * ((ntm + 127) / 128), K, spS, kpS);
         }
+        // workspace: A side first (VA, lineA, tmaxA: independent of N, so a chunked caller can
+        // reuse them), then the B side, then the checksum-GEMM partials
+        // (every sub-array starts on a 128-byte boundary: bulk copies and TMA need >= 16 B)
+        auto al = [](size_t n) { return (n + 15) / 16 * 16; };
+        const size_t oLA = al((size_t)ntm * Kp), oTA = oLA + al((size_t)kch * M), oWB = oTA + al((size_t)kch * ntm);
+        const size_t oLB = oWB + al((size_t)ntn * Kp), oTB = oLB + al((size_t)kch * N), oR = oTB + al((size_t)kch * ntn);
+        const size_t oS = oR + (pre ? al((size_t)spR * ntn * M) : 0);
+        const size_t need = (oS + (pre ? al((size_t)spS * ntm * N) : 0)) * sizeof(double);
         const size_t nRS = pre ? (size_t)spR * ntn * M + (size_t)spS * ntm * N : 0;
-        CK(c.ws.ensure((nV + nLine + nT + nRS) * sizeof(double)), "cudaMalloc(workspace)");
+        if (need > c.ws.bytes) c.ws_gen++;
+        CK(c.ws.ensure(need), "cudaMalloc(workspace)");
         double *w = c.ws.as<double>();
-        g.VA = w; g.WB = w + ntm * Kp;
-        double *lineA = w + nV, *lineB = lineA + (size_t)kch * M;
-        double *tmaxA = lineB + (size_t)kch * N, *tmaxB = tmaxA + (size_t)kch * ntm;
+        g.VA = w;
+        double *lineA = w + oLA, *tmaxA = w + oTA;
+        g.WB = w + oWB;
+        double *lineB = w + oLB, *tmaxB = w + oTB;
         g.lineA = lineA; g.lineB = lineB; g.tmaxA = tmaxA; g.tmaxB = tmaxB;
         g.kch = kch; g.Kp = Kp;
-        double *Rpre = tmaxB + (size_t)kch * ntn, *Spre = Rpre + (size_t)spR * ntn * M;
+        double *Rpre = w + oR, *Spre = w + oS;
         g.Rpre = pre ? Rpre : nullptr;
         g.Spre = pre ? Spre : nullptr;
         g.splits_r = (int)spR; g.splits_s = (int)spS;
@@ -398,12 +429,17 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
         rc = prepare_plan(M, N, off_i, off_j, g);
         if (rc) return rc;
         EncodeArgs ea{};
-        ea.op[0] = EncodeOperand{A, lda, M, kca ? 1 : 0, va ? 1 : 0, const_cast<double *>(g.VA), lineA, tmaxA, (int)ntm};
-        ea.op[1] = EncodeOperand{B, ldb, N, kcb ? 1 : 0, vb ? 1 : 0, const_cast<double *>(g.WB), lineB, tmaxB, (int)ntn};
+        const EncodeOperand opA{A, lda, M, kca ? 1 : 0, va ? 1 : 0, const_cast<double *>(g.VA), lineA, tmaxA, (int)ntm};
+        const EncodeOperand opB{B, ldb, N, kcb ? 1 : 0, vb ? 1 : 0, const_cast<double *>(g.WB), lineB, tmaxB, (int)ntn};
+        ea.op[0] = skip_a ? opB : opA;
+        ea.op[1] = opB;
         ea.K = (alpha == 0.0) ? 0 : K;  // alpha == 0: A, B are not read (encodes are zero)
         ea.Kp = Kp; ea.kper = kper; ea.kch = kch; ea.rep = append ? nullptr : g.rep;
-        dim3 grid((unsigned)std::max(ntm, ntn), (unsigned)kch, 2);
+        dim3 grid((unsigned)(skip_a ? ntn : std::max(ntm, ntn)), (unsigned)kch, skip_a ? 1 : 2);
         encode_kernel<<<grid, NTHREADS, 0, c.stream>>>(ea);
+        if (!skip_a) {
+            c.a_valid = true; c.a_key = akey; c.a_kch = kch; c.a_ws_gen = c.ws_gen;
+        }
         c.launches++;
         CK(cudaGetLastError(), "encode_kernel launch");
         if (pre && K > 0 && alpha != 0.0) {
@@ -411,14 +447,22 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
             // tensor cores:  R (M x ntn, ld M)   = op(A) . WB^T   [WB^T: k x ntn, 'N', ld Kp]
             //                S^T (N x ntm, ld N) = op(B)^T . VA^T [VA^T: k x ntm, 'N', ld Kp]
             // (column blocks of <= 128 tiles; k-split partials summed in the FT_PRE epilogue)
+            // R on the library stream and S^T on a forked side stream run concurrently (their
+            // CTAs share the waves), joined before the main GEMM
+            CK(c.ensure_copy_streams(), "streams");
+            CK(cudaEventRecord(c.ev_fork, c.stream), "event");
+            CK(cudaStreamWaitEvent(c.s_side, c.ev_fork, 0), "wait");
             for (long long q0 = 0; q0 < ntn; q0 += 128)
                 CK(cksum_gemm(kca, A, lda, M, g.WB + q0 * Kp, Kp, std::min<long long>(128, ntn - q0), K, spR, kpR,
                               Rpre + q0 * M, ntn * M, c.stream), "checksum GEMM R");
             for (long long q0 = 0; q0 < ntm; q0 += 128)
                 CK(cksum_gemm(kcb, B, ldb, N, g.VA + q0 * Kp, Kp, std::min<long long>(128, ntm - q0), K, spS, kpS,
-                              Spre + q0 * N, ntm * N, c.stream), "checksum GEMM S");
+                              Spre + q0 * N, ntm * N, c.s_side), "checksum GEMM S");
+            CK(cudaEventRecord(c.ev_join, c.s_side), "event");
+            CK(cudaStreamWaitEvent(c.stream, c.ev_join, 0), "wait");
         } else if (pre) {
-            CK(cudaMemsetAsync(Rpre, 0, nRS * sizeof(double), c.stream), "checksum zero");
+            CK(cudaMemsetAsync(Rpre, 0, (oS - oR + (size_t)spS * ntm * N) * sizeof(double), c.stream), "checksum zero");
+            (void)nRS;
         }
         if (c.profiling) CK(cudaEventRecord(rec.e1, c.stream), "event");
         if (pre)
@@ -452,9 +496,9 @@ int ftblas_dgemm_ex(char transA, char transB, int64_t M, int64_t N, int64_t K, d
                     int64_t row_offset, int64_t col_offset, int32_t flags, ftblas_err_report *err_report) {
     if (row_offset < 0 || row_offset % FTBLAS_TILE_M) return arg_fail(14, "row_offset not a multiple of the tile");
     if (col_offset < 0 || col_offset % FTBLAS_TILE_N) return arg_fail(15, "col_offset not a multiple of the tile");
-    if (flags & ~FTBLAS_REPORT_APPEND) return arg_fail(16, "unknown flags");
+    if (flags & ~(FTBLAS_REPORT_APPEND | FTBLAS_REUSE_A_ENCODE)) return arg_fail(16, "unknown flags");
     return dgemm_impl(true, transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, err_report, row_offset,
-                      col_offset, (flags & FTBLAS_REPORT_APPEND) != 0);
+                      col_offset, (flags & FTBLAS_REPORT_APPEND) != 0, (flags & FTBLAS_REUSE_A_ENCODE) != 0);
 }
 
 int ftblas_report_reset(void) {
@@ -521,7 +565,7 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
         const double *dB = readAB ? (is_t(transB) ? c.hB.as<double>() + c0 : c.hB.as<double>() + c0 * dlb) : nullptr;
         rc = dgemm_impl(true, transA, transB, M, n, K, alpha, readAB ? c.hA.as<double>() : nullptr,
                         readAB ? dla : std::max<long long>(1, ar), dB, readAB ? dlb : std::max<long long>(1, br),
-                        beta, c.hC.as<double>() + c0 * dlc, dlc, nullptr, 0, c0, q > 0);
+                        beta, c.hC.as<double>() + c0 * dlc, dlc, nullptr, 0, c0, q > 0, q > 0);
         if (rc) return rc;
         CK(cudaEventRecord(c.ev_done[q], c.stream), "event");
         CK(cudaStreamWaitEvent(c.s_down, c.ev_done[q], 0), "wait");
@@ -602,7 +646,7 @@ const char *ftblas_last_error(void) { return ctx().err; }
 int ftblas_release(void) {
     Ctx &c = ctx();
     cudaStreamSynchronize(c.stream);
-    c.ws.release(); c.rep.release(); c.plan_dev.release(); c.plan_ptr_dev.release();
+    c.ws.release(); c.ws_gen++; c.a_valid = false; c.rep.release(); c.plan_dev.release(); c.plan_ptr_dev.release();
     c.plan_uploaded = -1;
     c.hA.release(); c.hB.release(); c.hC.release();
     return 0;

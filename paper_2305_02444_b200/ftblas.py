@@ -87,6 +87,7 @@ EXPORTS = ("ftblas_dgemm", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_rep
            "ftblas_dgemm_ex", "ftblas_report_reset")
 
 REPORT_APPEND = 1  # FTBLAS_REPORT_APPEND
+REUSE_A_ENCODE = 2  # FTBLAS_REUSE_A_ENCODE
 
 CHECKSUM_GEMM = 0   # FTBLAS_CHECKSUM_GEMM: checksum row/column by two DMMA GEMMs (default)
 CHECKSUM_FUSED = 1  # FTBLAS_CHECKSUM_FUSED: accumulated in the main GEMM's mainloop
@@ -154,11 +155,11 @@ def ftblas_dgemm(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, r
 
 
 def ftblas_dgemm_ex(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, row_offset=0,
-                    col_offset=0, append=False, report=None):
+                    col_offset=0, append=False, report=None, reuse_a=False):
     rep = ct.byref(report.c) if report is not None else None
+    flags = (REPORT_APPEND if append else 0) | (REUSE_A_ENCODE if reuse_a else 0)
     _check(lib.ftblas_dgemm_ex(_tc(transA), _tc(transB), M, N, K, alpha, _ptr(A), lda, _ptr(B), ldb,
-                               beta, _ptr(C), ldc, row_offset, col_offset,
-                               REPORT_APPEND if append else 0, rep))
+                               beta, _ptr(C), ldc, row_offset, col_offset, flags, rep))
     return report
 
 

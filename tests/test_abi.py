@@ -108,7 +108,7 @@ def test_checksum_mode_api(lib):
 
 
 @pytest.mark.parametrize("roff,coff,flags,code", [(64, 0, 0, -14), (-128, 0, 0, -14), (0, 5, 0, -15),
-                                                  (0, 0, 2, -16)])
+                                                  (0, 0, 4, -16)])
 def test_ex_argument_errors(lib, roff, coff, flags, code):
     """ftblas_dgemm_ex rejects offsets that are not whole tiles and unknown flags before any
     CUDA call (so this runs without a GPU)."""

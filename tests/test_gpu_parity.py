@@ -231,10 +231,11 @@ def test_blocked_calls_with_offsets_and_append(ft, split):
     A_t, pA = to_dev(d["A"]); B_t, pB = to_dev(d["B"]); C_t, pC = to_dev(d["C"])
     ft.ftblas_set_fault_plan(*plan)
     ft.ftblas_report_reset()
-    if split == "cols":
+    if split == "cols":  # later blocks reuse the A encoding (FTBLAS_REUSE_A_ENCODE)
         for q, (c0, c1) in enumerate([(0, 256), (256, 384), (384, 520)]):
             ft.ftblas_dgemm_ex("N", "N", w.M, c1 - c0, w.K, w.alpha, pA, d["lda"], pB + 8 * c0 * d["ldb"],
-                               d["ldb"], w.beta, pC + 8 * c0 * d["ldc"], d["ldc"], 0, c0, q > 0)
+                               d["ldb"], w.beta, pC + 8 * c0 * d["ldc"], d["ldc"], 0, c0, q > 0,
+                               reuse_a=q > 0)
     else:
         for q, (r0, r1) in enumerate([(0, 128), (128, 400)]):
             ft.ftblas_dgemm_ex("N", "N", r1 - r0, w.N, w.K, w.alpha, pA + 8 * r0, d["lda"], pB, d["ldb"],
