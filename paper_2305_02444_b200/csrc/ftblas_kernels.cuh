@@ -420,8 +420,8 @@ __global__ void __launch_bounds__(NTHREADS) encode_kernel(EncodeArgs a) {
 // ------------------------------------------------------------------ GEMM kernel
 constexpr int LDT = 130;  // epilogue tile leading dimension (conflict-free fragment stores)
 constexpr int EPI_EL = 128 * LDT   /* tile */
-                     + 6 * 128     /* rowS[2][128], rowC[2][128], rowCA[2][128] */
-                     + 3 * 128     /* colS, colC, colCA */
+                     + 12 * 128    /* red_r[4][3][128] */
+                     + 6 * 128     /* red_c[2][3][128] */
                      + 2 * 256     /* rsp[128], ssp[128] (+ spare) */
                      + 128         /* row residuals */
                      + 136;        /* flags (int) */
@@ -758,10 +758,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
 
     // -------------------------------------------------------------- FT epilogue
-    double *rowS = tileS + 128 * LDT;        // [2][128]
-    double *rowC = rowS + 256, *rowCA = rowC + 256;
-    double *colS = rowCA + 256, *colC = colS + 128, *colCA = colC + 128;
-    double *rsp = colCA + 128, *ssp = rsp + 256, *dres = ssp + 256;
+    // partial row sums [wn][q][128] and column sums [wm][q][128], q = 0: out, 1: C0, 2: |C0|
+    double *red_r = tileS + 128 * LDT;       // 4 x 3 x 128
+    double *red_c = red_r + 4 * 3 * 128;     // 2 x 3 x 128
+    double *rsp = red_c + 2 * 3 * 128, *ssp = rsp + 256, *dres = ssp + 256;
     int *flags = reinterpret_cast<int *>(dres + 128);  // [0] nrow, [1] ncol, [2..129] rows, [130..257] cols
 
     // checksum reference: FUSED -- combine the 4 k-lanes of the mainloop partials (fixed order),
@@ -786,32 +786,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     if (tid == 0) { flags[0] = 0; flags[1] = 0; }
 
-    // C0 tile -> smem, then its row/column sums (the beta C encoding)
-    const int rr = tid & 127, hh = tid >> 7;
+    // C0 tile -> smem (all loads in flight at once)
     if (!beta0) {
         stage_c0();
-        bar_mma();
-        double s = 0.0, sa = 0.0;
-        for (int c = hh * 64; c < hh * 64 + 64; c++) {
-            const double v = tileS[rr + c * LDT];
-            s += v; sa += fabs(v);
-        }
-        rowC[hh * 128 + rr] = s; rowCA[hh * 128 + rr] = sa;
-        for (int q = 0; q < 16; q++) {
-            const int c = warp * 16 + q;
-            double cs = 0.0, ca = 0.0;
-#pragma unroll
-            for (int r4 = 0; r4 < 4; r4++) {
-                const double v = tileS[lane + 32 * r4 + c * LDT];
-                cs += v; ca += fabs(v);
-            }
-#pragma unroll
-            for (int off = 16; off; off >>= 1) {
-                cs += __shfl_xor_sync(0xffffffffu, cs, off);
-                ca += __shfl_xor_sync(0xffffffffu, ca, off);
-            }
-            if (lane == 0) { colC[c] = cs; colCA[c] = ca; }
-        }
         bar_mma();
     }
     // fault injection (test harness): flip accumulator bits of planned elements of this tile
@@ -831,22 +808,61 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     }
         }
     }
-    form_out();
-    bar_mma();
-    // row / column sums of the computed tile (warp-shuffle reductions for the columns)
+    // One pass over this thread's fragment elements: out = alpha acc + beta C0 into the smem
+    // tile (0 outside M x N), with the row sums (over the thread's 8 columns of a fragment
+    // row, then the 4 lanes of the row) and column sums (over the thread's 8 rows, then the
+    // 8 lanes of the column) of out, C0 and |C0| -- the reference sums of the computed tile
+    // (formed "at register level") and the beta C encoding (reading R3).
     {
-        double s = 0.0;
-        for (int c = hh * 64; c < hh * 64 + 64; c++) s += tileS[rr + c * LDT];
-        rowS[hh * 128 + rr] = s;
-        for (int q = 0; q < 16; q++) {
-            const int c = warp * 16 + q;
-            double cs = 0.0;
+        double cs[FN][2], cc[FN][2], ca[FN][2];
 #pragma unroll
-            for (int r4 = 0; r4 < 4; r4++) cs += tileS[lane + 32 * r4 + c * LDT];
+        for (int b = 0; b < FN; b++) cs[b][0] = cs[b][1] = cc[b][0] = cc[b][1] = ca[b][0] = ca[b][1] = 0.0;
+        auto row_red = [&](double v, int q, int row) {
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            if ((lane & 3) == 0) red_r[(wn * 3 + q) * 128 + row] = v;
+        };
 #pragma unroll
-            for (int off = 16; off; off >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, off);
-            if (lane == 0) colS[c] = cs;
+        for (int a = 0; a < FM; a++) {
+            const int row = row_of(a);
+            double rs = 0.0, rc = 0.0, ra = 0.0;
+#pragma unroll
+            for (int b = 0; b < FN; b++)
+#pragma unroll
+                for (int e = 0; e < 2; e++) {
+                    const int col = col_of(b, e);
+                    const bool ok = row < mvalid && col < nvalid;
+                    double o;
+                    if (beta0) {
+                        o = g.alpha * acc[a][b][e];
+                    } else {
+                        const double c0 = tileS[row + col * LDT];  // 0 outside M x N (zero-filled)
+                        o = fma(g.alpha, acc[a][b][e], g.beta * c0);
+                        rc += c0; ra += fabs(c0);
+                        cc[b][e] += c0; ca[b][e] += fabs(c0);
+                    }
+                    o = ok ? o : 0.0;
+                    tileS[row + col * LDT] = o;
+                    rs += o;
+                    cs[b][e] += o;
+                }
+            row_red(rs, 0, row);
+            if (!beta0) { row_red(rc, 1, row); row_red(ra, 2, row); }
         }
+        auto col_red = [&](double (&v)[FN][2], int q) {
+#pragma unroll
+            for (int b = 0; b < FN; b++)
+#pragma unroll
+                for (int e = 0; e < 2; e++) {
+                    double x = v[b][e];
+                    x += __shfl_xor_sync(0xffffffffu, x, 4);
+                    x += __shfl_xor_sync(0xffffffffu, x, 8);
+                    x += __shfl_xor_sync(0xffffffffu, x, 16);
+                    if (lane < 4) red_c[(wm * 3 + q) * 128 + col_of(b, e)] = x;
+                }
+        };
+        col_red(cs, 0);
+        if (!beta0) { col_red(cc, 1); col_red(ca, 2); }
     }
     bar_mma();
     // verification: flag rows / columns beyond the round-off threshold
@@ -855,10 +871,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (tid < 128) {
         const int r = tid;
         if (r < mvalid) {
-            const double sum = rowS[r] + rowS[128 + r];
+            auto rsum = [&](int q) {
+                return ((red_r[(0 * 3 + q) * 128 + r] + red_r[(1 * 3 + q) * 128 + r]) + red_r[(2 * 3 + q) * 128 + r]) +
+                       red_r[(3 * 3 + q) * 128 + r];
+            };
+            const double sum = rsum(0);
             const double rr2 = FUSED ? rsp[r] : pre_r[r];
-            const double c0s = beta0 ? 0.0 : rowC[r] + rowC[128 + r];
-            const double c0a = beta0 ? 0.0 : rowCA[r] + rowCA[128 + r];
+            const double c0s = beta0 ? 0.0 : rsum(1);
+            const double c0a = beta0 ? 0.0 : rsum(2);
             const double ref = beta0 ? g.alpha * rr2 : fma(g.alpha, rr2, g.beta * c0s);
             const double rowabs = nrm_row[r], bmax = nrm_max[1];
             const double tau = 4.0 * U_ROUND * (double)(g.K + nvalid + 3) * (aa * rowabs * bmax + ab * c0a);
@@ -872,10 +892,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     } else {
         const int c = tid - 128;
         if (c < nvalid) {
-            const double sum = colS[c];
+            auto csum = [&](int q) { return red_c[(0 * 3 + q) * 128 + c] + red_c[(1 * 3 + q) * 128 + c]; };
+            const double sum = csum(0);
             const double ss2 = FUSED ? ssp[c] : pre_s[c];
-            const double c0s = beta0 ? 0.0 : colC[c];
-            const double c0a = beta0 ? 0.0 : colCA[c];
+            const double c0s = beta0 ? 0.0 : csum(1);
+            const double c0a = beta0 ? 0.0 : csum(2);
             const double ref = beta0 ? g.alpha * ss2 : fma(g.alpha, ss2, g.beta * c0s);
             const double colabs = nrm_col[c], amax = nrm_max[0];
             const double tau = 4.0 * U_ROUND * (double)(g.K + mvalid + 3) * (aa * amax * colabs + ab * c0a);
