@@ -197,6 +197,10 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned b
                      smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b))
                  : "memory");
 }
+// L2 prefetch of `bytes` (multiple of 16, 16-byte aligned source) -- no smem, no completion
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bar_mma() {  // named barrier over the NTHREADS MMA threads only
     asm volatile("bar.sync 1, %0;\n" ::"n"(NTHREADS) : "memory");
 }
@@ -610,6 +614,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (ALL_TMA) {
             if (pt != 0) return;
             for (int kt = 0; kt < ktiles; kt++) {
+                if (kt == STAGES && g.beta != 0.0 && g.vecC) {
+                    // C0 of this tile -> L2 while the mainloop runs (the epilogue stages it into
+                    // smem afterwards); after the first stages so it does not delay them
+                    const unsigned bytes = (unsigned)(min((long long)BM, g.M - m0) * 8) & ~15u;
+                    const long long nv = min((long long)BN, g.N - n0);
+                    if (bytes)
+                        for (int c = 0; c < nv; c++) bulk_prefetch_l2(g.C + m0 + (n0 + c) * g.ldc, bytes);
+                }
                 if (kt >= STAGES) mbar_wait(&empty_bar[kt % STAGES], ((kt / STAGES) - 1) & 1);
                 produce(kt);
             }
