@@ -173,6 +173,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=list(syn.CONFIG_BY_NAME))
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: functional check of the multi-rank "
+                         "path on fewer GPUs than ranks; not a performance configuration)")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     args = ap.parse_args()
@@ -189,9 +192,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     stream = torch.cuda.current_stream()
     fb.ftblas_set_stream(stream)
     fb.ftblas_set_checksum_mode("gemm")
@@ -203,14 +209,14 @@ def main():
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if args.backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if args.backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
@@ -248,7 +254,7 @@ def main():
 
     # N > 1: op(B) is broadcast in column chunks of whole tiles, the GEMM of chunk c overlapping
     # the broadcast of chunks > c (shard.sharded_dgemm); N = 1: one call, no exchange.
-    chunks = 8 if world > 1 else 1
+    chunks = 8 if (world > 1 and w.transB == "N") else 1
 
     def step(gemm, broadcast):
         # C := alpha AB + beta C accumulates into C; the value drifts but the work is identical
@@ -375,8 +381,8 @@ def main():
                        "injected_flips": w.n_flips, "flip_bits": [syn.BIT_LO, syn.BIT_HI],
                        "verification_tile": [syn.TILE_M, syn.TILE_N],
                        "parallelism": f"row-block x{world}" + (
-                           f", op(B) NCCL broadcast per step in {chunks} column chunks overlapped with the GEMM"
-                           if world > 1 else ""),
+                           (f", op(B) {args.backend.upper()} broadcast per step in {chunks} column chunks overlapped with the GEMM"
+                            if chunks > 1 else f", op(B) {args.backend.upper()} broadcast per step") if world > 1 else ""),
                        "l2": "no flush: operands (%.1f GiB) >> 126 MB L2" % ((d["A"].nbytes + d["B"].nbytes + d["C"].nbytes) / 2**30)},
             "fp64_peak_tflops": FP64_PEAK_TFLOPS,
             "pct_fp64_peak": 100.0 * value / (FP64_PEAK_TFLOPS * world),
