@@ -36,6 +36,19 @@ DEFAULT_WORKLOAD = "c3_16384_sharded"
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 
 
+def ratio_rule(achieved: float) -> dict:
+    """The contraction peak by the task's ratio rule: measured bf16 (MEASURED_PEAKS.json) x the
+    nominal FP64 / bf16 ratio of B200 (45 / 2250 TFLOP/s).  Reported beside the DMMA-measured
+    peak used for `frac` (the rule's figure is below what cuBLAS DGEMM reaches on these GPUs)."""
+    try:
+        bf16 = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
+        src = "MEASURED_PEAKS.json bf16_tflops"
+    except (OSError, ValueError, KeyError):
+        bf16, src = 1590.0, "fallback 1.59 PFLOP/s (B200_PROFILING.md)"
+    peak = bf16 * 45.0 / 2250.0
+    return {"peak": peak, "frac": achieved / peak, "how": f"{src} {bf16:.1f} x 45/2250"}
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -399,7 +412,8 @@ def main():
                          "kernel": "gemm_kernel<FT_PRE> (TMA + DMMA mainloop, verify/locate/correct epilogue)",
                          "kernel_ms": gemm_avg_ms,
                          "checksum_stage_ms": enc_avg_ms,
-                         "peak_source": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DMMA microbench 37.15, profiles/r01_fp64_pipes.txt)"},
+                         "peak_source": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DMMA microbench 37.15, profiles/r01_fp64_pipes.txt)",
+                         "peak_ratio_rule": ratio_rule(achieved)},
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,

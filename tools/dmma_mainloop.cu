@@ -265,6 +265,66 @@ int run_cw(const char *name, int sms, double *out) {
     return 0;
 }
 
+
+// CTA tile 128 x (32 * NWN) with 2 x NWN warps of 64 x 32; minBlocks CTAs per SM requested.
+template <int NWN, int MINB>
+__global__ void __launch_bounds__(64 * NWN, MINB) mainloop_nw(double *out, int ktiles) {
+    extern __shared__ double smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 1, wn = warp >> 1;
+    constexpr int BNT = 32 * NWN, A_EL = BK * LD_MN, B_EL = BNT * LD_K, ST = A_EL + B_EL;
+    for (int i = tid; i < STAGES * ST; i += blockDim.x) smem[i] = 1.0 + 1e-3 * (i & 63);
+    __syncthreads();
+    double acc[8][4][2];
+#pragma unroll
+    for (int a = 0; a < 8; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int kt = 0; kt < ktiles; kt++) {
+        const double *as = smem + (kt % STAGES) * ST, *bs = as + A_EL;
+#pragma unroll
+        for (int kk = 0; kk < BK / 4; kk++) {
+            double af[8], bf[4];
+            const int k = kk * 4 + (lane & 3);
+#pragma unroll
+            for (int f = 0; f < 8; f++) af[f] = as[k * LD_MN + wm * 64 + f * 8 + (lane >> 2)];
+#pragma unroll
+            for (int f = 0; f < 4; f++) bf[f] = bs[(wn * 32 + f * 8 + (lane >> 2)) * LD_K + k];
+#pragma unroll
+            for (int a = 0; a < 8; a++)
+#pragma unroll
+                for (int b = 0; b < 4; b++) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        }
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a < 8; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) s += acc[a][b][0] + acc[a][b][1];
+    out[blockIdx.x * blockDim.x + tid] = s;
+}
+
+template <int NWN, int MINB>
+int run_nw(const char *name, int sms, double *out, int blocks_per_sm, int stages_bytes_div) {
+    auto k = mainloop_nw<NWN, MINB>;
+    const int bytes = STAGES * (BK * LD_MN + 32 * NWN * LD_K) * 8;
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    const int ktiles = 4096, blocks = sms * blocks_per_sm * 4;
+    k<<<blocks, 64 * NWN, bytes>>>(out, 64);
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    k<<<blocks, 64 * NWN, bytes>>>(out, ktiles);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    const double fl = 2.0 * 128 * 32 * NWN * BK * (double)ktiles * blocks;
+    printf("%-34s %8.3f ms  %6.2f TFLOP/s\n", name, ms, fl / ms / 1e9);
+    (void)stages_bytes_div;
+    return 0;
+}
+
 int main() {
     cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
     printf("device %s sms=%d\n", p.name, p.multiProcessorCount);
@@ -276,6 +336,9 @@ int main() {
     run<5, 64, 32>("+DFMA interleaved 16/k4x8 (regs)", sms, out);
     run<6, 64, 32>("+frag-reuse 4 DFMA/k4 + 2 LDS/k4", sms, out);
     run<7, 64, 32>("+frag-reuse 4 DFMA/k4 (no LDS)", sms, out);
+    run_nw<4, 1>("8 warps 128x128, 1 CTA/SM", sms, out, 1, 1);
+    run_nw<2, 1>("4 warps 128x64, 1 CTA/SM", sms, out, 1, 1);
+    run_nw<2, 2>("4 warps 128x64, 2 CTA/SM", sms, out, 2, 1);
     run_cw<4, 0>("8 MMA + 4 cksum warps LDS+DFMA", sms, out);
     run_cw<4, 1>("8 MMA + 4 cksum warps LDS only", sms, out);
     run_cw<4, 2>("8 MMA + 4 cksum warps DFMA only", sms, out);
