@@ -51,7 +51,7 @@ struct Ctx {
     DevBuf hA, hB, hC;    // ftblas_dgemm_host device staging
     cudaStream_t s_up = nullptr, s_down = nullptr;  // ftblas_dgemm_host copy streams
     cudaStream_t s_side = nullptr;                   // checksum GEMM S^T (forked / joined)
-    cudaEvent_t ev_entry = nullptr, ev_exit = nullptr, ev_up[8] = {}, ev_done[8] = {};
+    cudaEvent_t ev_entry = nullptr, ev_exit = nullptr, ev_up[8] = {}, ev_done[16] = {}, ev_a[2] = {};
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // cached A-side encoding (FTBLAS_REUSE_A_ENCODE)
     struct AKey {
@@ -73,10 +73,9 @@ struct Ctx {
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_entry, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_exit, cudaEventDisableTiming);
-        for (int q = 0; q < 8 && e == cudaSuccess; q++) {
-            e = cudaEventCreateWithFlags(&ev_up[q], cudaEventDisableTiming);
-            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_done[q], cudaEventDisableTiming);
-        }
+        for (int q = 0; q < 8 && e == cudaSuccess; q++) e = cudaEventCreateWithFlags(&ev_up[q], cudaEventDisableTiming);
+        for (int q = 0; q < 16 && e == cudaSuccess; q++) e = cudaEventCreateWithFlags(&ev_done[q], cudaEventDisableTiming);
+        for (int q = 0; q < 2 && e == cudaSuccess; q++) e = cudaEventCreateWithFlags(&ev_a[q], cudaEventDisableTiming);
         return e;
     }
     long long launches = 0;
@@ -533,44 +532,86 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
     }
     CK(c.hC.ensure((size_t)dlc * N * 8), "cudaMalloc(C)");
     CK(c.ensure_copy_streams(), "copy streams");
-    // Pipeline over column blocks of whole tiles: op(A) first (every block needs it), then per
-    // block the H2D of its op(B) columns (rows of B for 'T') and C0 columns on the upload
-    // stream, its ABFT GEMM on the library stream (report appended, block column offset), and
-    // the D2H of its verified C columns on the download stream -- the PCIe traffic of the
-    // later blocks overlaps the DMMA work of the earlier ones, both directions at once.
-    const long long tiles_n = (N + FTBLAS_TILE_N - 1) / FTBLAS_TILE_N;
-    const long long nblk = std::min<long long>(tiles_n, 8);
+    // Pipeline over blocks of whole tiles: nrb row blocks x ncb column blocks.  The upload
+    // stream carries op(A) row block 0, then every op(B) column block (rows of B for 'T') with
+    // the C0 block it completes, then the other op(A) row blocks and their C0 blocks; the
+    // library stream runs block (rb, cb) as soon as its three uploads have landed
+    // (ftblas_dgemm_ex semantics: caller coordinates, report appended, A encoding reused along
+    // a row block); the download stream returns each verified C block.  PCIe traffic in both
+    // directions overlaps the DMMA work; only op(A) row block 0 and op(B) block 0 are exposed.
+    const long long tiles_m = (M + FTBLAS_TILE_M - 1) / FTBLAS_TILE_M, tiles_n = (N + FTBLAS_TILE_N - 1) / FTBLAS_TILE_N;
+    const long long T = tiles_m * tiles_n;
+    const long long nrb = (T / 600 >= 4 && tiles_m >= 16) ? 2 : 1;  // 2 row blocks once >= 4 waves each
+    const long long ncb = std::min<long long>(8, tiles_n);
+    auto split = [](long long tiles, long long nb, long long q, long long tile, long long lim, long long &x0,
+                    long long &x1) {
+        const long long per = tiles / nb, rem = tiles % nb;
+        const long long t0 = q * per + std::min(q, rem), t1 = t0 + per + (q < rem ? 1 : 0);
+        x0 = t0 * tile;
+        x1 = std::min(lim, t1 * tile);
+    };
     CK(cudaEventRecord(c.ev_entry, c.stream), "event");  // device buffers free once prior work is done
     CK(cudaStreamWaitEvent(c.s_up, c.ev_entry, 0), "wait");
-    if (readAB)
-        CK(cudaMemcpy2DAsync(c.hA.p, dla * 8, A, lda * 8, ar * 8, ac, cudaMemcpyHostToDevice, c.s_up), "H2D A");
-    long long t0 = 0;
-    for (long long q = 0; q < nblk; q++) {
-        const long long t1 = t0 + tiles_n / nblk + (q < tiles_n % nblk ? 1 : 0);
-        const long long c0 = t0 * FTBLAS_TILE_N, c1 = std::min<long long>(N, t1 * FTBLAS_TILE_N), n = c1 - c0;
-        t0 = t1;
+    double *dA = c.hA.as<double>(), *dB = c.hB.as<double>(), *dC = c.hC.as<double>();
+    auto up_A = [&](long long rb) -> cudaError_t {
+        long long r0, r1;
+        split(tiles_m, nrb, rb, FTBLAS_TILE_M, M, r0, r1);
+        if (!readAB) return cudaSuccess;
+        if (is_t(transA))  // op(A)(r0:r1, :) = columns r0..r1 of the K x M stored A
+            return cudaMemcpy2DAsync(dA + r0 * dla, dla * 8, A + r0 * lda, lda * 8, K * 8, r1 - r0,
+                                     cudaMemcpyHostToDevice, c.s_up);
+        return cudaMemcpy2DAsync(dA + r0, dla * 8, A + r0, lda * 8, (r1 - r0) * 8, K, cudaMemcpyHostToDevice, c.s_up);
+    };
+    auto up_C0 = [&](long long rb, long long cb) -> cudaError_t {
+        long long r0, r1, c0, c1;
+        split(tiles_m, nrb, rb, FTBLAS_TILE_M, M, r0, r1);
+        split(tiles_n, ncb, cb, FTBLAS_TILE_N, N, c0, c1);
+        if (beta == 0.0) return cudaSuccess;
+        return cudaMemcpy2DAsync(dC + r0 + c0 * dlc, dlc * 8, C + r0 + c0 * ldc, ldc * 8, (r1 - r0) * 8, c1 - c0,
+                                 cudaMemcpyHostToDevice, c.s_up);
+    };
+    CK(up_A(0), "H2D A");
+    CK(cudaEventRecord(c.ev_a[0], c.s_up), "event");
+    for (long long cb = 0; cb < ncb; cb++) {
+        long long c0, c1;
+        split(tiles_n, ncb, cb, FTBLAS_TILE_N, N, c0, c1);
         if (readAB) {
             if (is_t(transB))  // op(B)(:, c0:c1) = rows c0..c1 of the N x K stored B
-                CK(cudaMemcpy2DAsync(c.hB.as<double>() + c0, dlb * 8, B + c0, ldb * 8, n * 8, K,
-                                     cudaMemcpyHostToDevice, c.s_up), "H2D B");
+                CK(cudaMemcpy2DAsync(dB + c0, dlb * 8, B + c0, ldb * 8, (c1 - c0) * 8, K, cudaMemcpyHostToDevice,
+                                     c.s_up), "H2D B");
             else
-                CK(cudaMemcpy2DAsync(c.hB.as<double>() + c0 * dlb, dlb * 8, B + c0 * ldb, ldb * 8, K * 8, n,
+                CK(cudaMemcpy2DAsync(dB + c0 * dlb, dlb * 8, B + c0 * ldb, ldb * 8, K * 8, c1 - c0,
                                      cudaMemcpyHostToDevice, c.s_up), "H2D B");
         }
-        if (beta != 0.0)
-            CK(cudaMemcpy2DAsync(c.hC.as<double>() + c0 * dlc, dlc * 8, C + c0 * ldc, ldc * 8, M * 8, n,
-                                 cudaMemcpyHostToDevice, c.s_up), "H2D C");
-        CK(cudaEventRecord(c.ev_up[q], c.s_up), "event");
-        CK(cudaStreamWaitEvent(c.stream, c.ev_up[q], 0), "wait");
-        const double *dB = readAB ? (is_t(transB) ? c.hB.as<double>() + c0 : c.hB.as<double>() + c0 * dlb) : nullptr;
-        rc = dgemm_impl(true, transA, transB, M, n, K, alpha, readAB ? c.hA.as<double>() : nullptr,
-                        readAB ? dla : std::max<long long>(1, ar), dB, readAB ? dlb : std::max<long long>(1, br),
-                        beta, c.hC.as<double>() + c0 * dlc, dlc, nullptr, 0, c0, q > 0, q > 0);
-        if (rc) return rc;
-        CK(cudaEventRecord(c.ev_done[q], c.stream), "event");
-        CK(cudaStreamWaitEvent(c.s_down, c.ev_done[q], 0), "wait");
-        CK(cudaMemcpy2DAsync(C + c0 * ldc, ldc * 8, c.hC.as<double>() + c0 * dlc, dlc * 8, M * 8, n,
-                             cudaMemcpyDeviceToHost, c.s_down), "D2H C");
+        CK(up_C0(0, cb), "H2D C");
+        CK(cudaEventRecord(c.ev_up[cb], c.s_up), "event");
+    }
+    for (long long rb = 1; rb < nrb; rb++) {
+        CK(up_A(rb), "H2D A");
+        for (long long cb = 0; cb < ncb; cb++) CK(up_C0(rb, cb), "H2D C");
+        CK(cudaEventRecord(c.ev_a[rb], c.s_up), "event");
+    }
+    for (long long rb = 0; rb < nrb; rb++) {
+        long long r0, r1;
+        split(tiles_m, nrb, rb, FTBLAS_TILE_M, M, r0, r1);
+        CK(cudaStreamWaitEvent(c.stream, c.ev_a[rb], 0), "wait");
+        const double *Ab = readAB ? (is_t(transA) ? dA + r0 * dla : dA + r0) : nullptr;
+        for (long long cb = 0; cb < ncb; cb++) {
+            long long c0, c1;
+            split(tiles_n, ncb, cb, FTBLAS_TILE_N, N, c0, c1);
+            if (rb == 0) CK(cudaStreamWaitEvent(c.stream, c.ev_up[cb], 0), "wait");
+            const double *Bb = readAB ? (is_t(transB) ? dB + c0 : dB + c0 * dlb) : nullptr;
+            const bool first = rb == 0 && cb == 0;
+            rc = dgemm_impl(true, transA, transB, r1 - r0, c1 - c0, K, alpha, Ab, readAB ? dla : std::max<long long>(1, ar),
+                            Bb, readAB ? dlb : std::max<long long>(1, br), beta, dC + r0 + c0 * dlc, dlc, nullptr, r0,
+                            c0, !first, cb > 0);
+            if (rc) return rc;
+            const int q = (int)(rb * ncb + cb);
+            CK(cudaEventRecord(c.ev_done[q], c.stream), "event");
+            CK(cudaStreamWaitEvent(c.s_down, c.ev_done[q], 0), "wait");
+            CK(cudaMemcpy2DAsync(C + r0 + c0 * ldc, ldc * 8, dC + r0 + c0 * dlc, dlc * 8, (r1 - r0) * 8, c1 - c0,
+                                 cudaMemcpyDeviceToHost, c.s_down), "D2H C");
+        }
     }
     CK(cudaEventRecord(c.ev_exit, c.s_down), "event");
     CK(cudaStreamWaitEvent(c.stream, c.ev_exit, 0), "wait");  // later library work sees C on the host

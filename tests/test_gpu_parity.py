@@ -196,7 +196,7 @@ def test_beta_zero_ignores_nan_in_C(ft):
     assert np.isfinite(C_gpu).all() and rep.count == 0
 
 
-@pytest.mark.parametrize("shape", ["c0", "blocks_nt", "blocks_ntn_ragged"])
+@pytest.mark.parametrize("shape", ["c0", "blocks_nt", "blocks_ntn_ragged", "rowblocks"])
 def test_host_buffer_entry_point(ft, shape):
     """The e2e call on host buffers: pipelined over column blocks (H2D / GEMM / D2H overlap),
     report accumulated over the blocks; must equal the oracle on the whole problem."""
@@ -204,8 +204,10 @@ def test_host_buffer_entry_point(ft, shape):
         w = syn.CONFIGS[0]
     elif shape == "blocks_nt":   # 9 column tiles -> 8 blocks, transposed B (2-D row-slab copies)
         w = syn.Workload("hb", 300, 1100, 60, "N", "T", -0.75, 1.5, "uniform", True, seed=31, n_flips=7)
-    else:                        # ragged last tile, transposed A, beta = 0
+    elif shape == "blocks_ntn_ragged":  # ragged last tile, transposed A, beta = 0
         w = syn.Workload("hb2", 130, 390, 33, "T", "N", 2.0, 0.0, "normal", True, seed=32, n_flips=3)
+    else:                        # 16 x 150 tiles: 2 row blocks x 8 column blocks, op(A) = A^T
+        w = syn.Workload("hb3", 2048, 19200, 16, "T", "N", 1.0, -1.0, "uniform", True, seed=33, n_flips=9)
     d = syn.make_inputs(w)
     plan = syn.fault_plan(w.M, w.N, w.n_flips, w.seed)
     ft.ftblas_set_fault_plan(*plan)
