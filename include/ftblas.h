@@ -150,6 +150,21 @@ int ftblas_set_fault_plan(int64_t n, const int64_t *i, const int64_t *j, const i
 int ftblas_set_checksum_mode(int mode);
 int ftblas_get_checksum_mode(void);
 
+/* CTA tiling of the GEMM kernels (a performance choice; results, reports and the 128 x 128
+ * verification tile are the same):
+ *   FTBLAS_TILES_AUTO (default): FTBLAS_TILES_PAIR for K <= 2048, else FTBLAS_TILES_FULL;
+ *   FTBLAS_TILES_FULL: one CTA per 128 x 128 tile (8 MMA warps, one CTA per SM);
+ *   FTBLAS_TILES_PAIR: two CTAs per tile, each a 128 x 64 half (4 MMA warps, two CTAs per SM so
+ *       one CTA's epilogue overlaps another's mainloop); for ftblas_dgemm the halves form a
+ *       thread-block cluster and exchange their row sums through distributed shared memory.
+ * The fused checksum mode always uses FTBLAS_TILES_FULL.  Returns 0, or -1 for an unknown
+ * policy. */
+#define FTBLAS_TILES_AUTO 0
+#define FTBLAS_TILES_FULL 1
+#define FTBLAS_TILES_PAIR 2
+int ftblas_set_tile_policy(int policy);
+int ftblas_get_tile_policy(void);
+
 /* Stream for subsequent calls (a cudaStream_t passed as void*; NULL = default stream). */
 int ftblas_set_stream(void *stream);
 

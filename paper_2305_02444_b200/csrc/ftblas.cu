@@ -84,6 +84,8 @@ struct Ctx {
     std::vector<Rec> recs, pool;
     char err[512] = "no error";
     int checksum_mode = FTBLAS_CHECKSUM_GEMM;
+    int tile_policy = FTBLAS_TILES_AUTO;
+    long long pair_kmax = 2048;  // FTBLAS_TILES_AUTO: half-tile CTAs for K <= pair_kmax
     int device = -1;
 };
 Ctx &ctx() {
@@ -129,23 +131,45 @@ int check_args(char ta, char tb, long long M, long long N, long long K, const vo
     return 0;
 }
 
-template <bool KCA, bool KCB, bool TMA, int MODE>
+// tiles = number of 128 x 128 tiles.  NWN = 4: one CTA per tile.  NWN = 2: two CTAs per tile
+// (128 x 64 halves, two resident per SM); for FT the halves of a tile form a cluster of 2.
+template <bool KCA, bool KCB, bool TMA, int MODE, int NWN>
 cudaError_t launch_gemm_t(const GemmArgs &g, const CUtensorMap &ma, const CUtensorMap &mb, long long tiles,
                           cudaStream_t s) {
-    auto kern = gemm_kernel<KCA, KCB, TMA, MODE>;
-    const int bytes = SmemPlan<MODE>::BYTES;
+    auto kern = gemm_kernel<KCA, KCB, TMA, MODE, NWN>;
+    const int bytes = SmemPlan<MODE, NWN>::BYTES;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)tiles, GEMM_THREADS, bytes, s>>>(g, ma, mb);
+    const unsigned threads = 64 * NWN + PRODUCER_THREADS;
+    if (NWN == 2) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e != cudaSuccess) return e;
+    }
+    if (NWN == 2 && MODE != MODE_NOFT) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)(2 * tiles), 1, 1);
+        cfg.blockDim = dim3(threads, 1, 1);
+        cfg.dynamicSmemBytes = bytes;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, kern, g, ma, mb);
+    } else {
+        kern<<<(unsigned)(NWN == 2 ? 2 * tiles : tiles), threads, bytes, s>>>(g, ma, mb);
+        e = cudaGetLastError();
+    }
     ctx().launches++;
-    return cudaGetLastError();
+    return e;
 }
 
-template <int MODE>
+template <int MODE, int NWN>
 cudaError_t launch_gemm(bool kca, bool kcb, bool tma, const GemmArgs &g, const CUtensorMap &ma,
                         const CUtensorMap &mb, long long tiles, cudaStream_t s) {
-    // 8 instantiations per mode: transpose layout x (TMA | cp.async fallback)
-#define L(a, b, c) if (kca == a && kcb == b && tma == c) return launch_gemm_t<a, b, c, MODE>(g, ma, mb, tiles, s)
+    // 8 instantiations per mode and tile width: transpose layout x (TMA | cp.async fallback)
+#define L(a, b, c) if (kca == a && kcb == b && tma == c) return launch_gemm_t<a, b, c, MODE, NWN>(g, ma, mb, tiles, s)
     L(false, true, true); L(false, false, true); L(true, true, true); L(true, false, true);
     L(false, true, false); L(false, false, false); L(true, true, false); L(true, false, false);
 #undef L
@@ -172,14 +196,15 @@ EncodeTiledFn encode_tiled() {
 // (mn contiguous): dims {MNd, Kd}, box {16, BK}; KC=true (k contiguous): dims {Kd, MNd}, box
 // {16, 128}.  128-byte swizzle, zero fill out of bounds.  Returns false when TMA cannot
 // describe the operand (the kernel then stages it with cp.async).
-bool make_operand_map(CUtensorMap *m, const double *X, long long ld, long long MNd, long long Kd, bool kc) {
+bool make_operand_map(CUtensorMap *m, const double *X, long long ld, long long MNd, long long Kd, bool kc,
+                      unsigned rows = 128) {
     std::memset(m, 0, sizeof(*m));
     EncodeTiledFn fn = encode_tiled();
     if (!fn || !X || MNd <= 0 || Kd <= 0 || (reinterpret_cast<uintptr_t>(X) & 15) || (ld & 1)) return false;
     if (MNd >= (1ll << 31) || Kd >= (1ll << 31)) return false;
     const cuuint64_t dims[2] = {(cuuint64_t)(kc ? Kd : MNd), (cuuint64_t)(kc ? MNd : Kd)};
     const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
-    const cuuint32_t box[2] = {16u, kc ? 128u : (cuuint32_t)BK};
+    const cuuint32_t box[2] = {16u, kc ? (cuuint32_t)rows : (cuuint32_t)BK};
     const cuuint32_t estr[2] = {1u, 1u};
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(X), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -282,11 +307,11 @@ struct Staging {
     bool tma;
 };
 Staging make_staging(const double *A, long long lda, long long M, bool kca, const double *B, long long ldb,
-                     long long N, bool kcb, long long K, double alpha) {
+                     long long N, bool kcb, long long K, double alpha, unsigned brows = 128) {
     Staging st;
     const bool use = K > 0 && alpha != 0.0;
     const bool ta = use && make_operand_map(&st.ma, A, lda, M, K, kca);
-    const bool tb = use && make_operand_map(&st.mb, B, ldb, N, K, kcb);
+    const bool tb = use && make_operand_map(&st.mb, B, ldb, N, K, kcb, brows);
     st.tma = ta && tb;
     if (!st.tma) { std::memset(&st.ma, 0, sizeof(st.ma)); std::memset(&st.mb, 0, sizeof(st.mb)); }
     return st;
@@ -370,7 +395,13 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
     g.M = M; g.N = N; g.K = K; g.alpha = alpha; g.beta = beta;
     const bool va = vec_ok(A, lda), vb = vec_ok(B, ldb);
     g.vecC = vec_ok(C, ldc) ? 1 : 0;  // 16-byte C0 staging / stores in every mode
-    const Staging stg = make_staging(A, lda, M, kca, B, ldb, N, kcb, K, alpha);
+    // tile policy: 128 x 64 half-tile CTAs (2 per SM, epilogue of one overlapping the mainloop of
+    // the other) when the per-tile mainloop is short, 128 x 128 CTAs otherwise; the fused
+    // checksum mode always uses 128 x 128
+    const bool fused = ft && c.checksum_mode == FTBLAS_CHECKSUM_FUSED;
+    const bool pair = !fused && (c.tile_policy == FTBLAS_TILES_PAIR ||
+                                 (c.tile_policy == FTBLAS_TILES_AUTO && K <= c.pair_kmax));
+    const Staging stg = make_staging(A, lda, M, kca, B, ldb, N, kcb, K, alpha, pair ? 64u : 128u);
     Ctx::Rec rec{};
     if (c.profiling) {
         rec = take_rec(ft);
@@ -404,7 +435,9 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
         const size_t oLA = al((size_t)ntm * Kp), oTA = oLA + al((size_t)kch * M), oWB = oTA + al((size_t)kch * ntm);
         const size_t oLB = oWB + al((size_t)ntn * Kp), oTB = oLB + al((size_t)kch * N), oR = oTB + al((size_t)kch * ntn);
         const size_t oS = oR + (pre ? al((size_t)spR * ntn * M) : 0);
-        const size_t need = (oS + (pre ? al((size_t)spS * ntm * N) : 0)) * sizeof(double);
+        const size_t oF = oS + (pre ? al((size_t)spS * ntm * N) : 0);  // finalized side data
+        const size_t nF = pre ? (size_t)(M + N + ntm + ntn) + (size_t)ntn * M + (size_t)ntm * N : 0;
+        const size_t need = (oF + nF) * sizeof(double);
         const size_t nRS = pre ? (size_t)spR * ntn * M + (size_t)spS * ntm * N : 0;
         if (need > c.ws.bytes) c.ws_gen++;
         CK(c.ws.ensure(need), "cudaMalloc(workspace)");
@@ -416,6 +449,9 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
         g.lineA = lineA; g.lineB = lineB; g.tmaxA = tmaxA; g.tmaxB = tmaxB;
         g.kch = kch; g.Kp = Kp;
         double *Rpre = w + oR, *Spre = w + oS;
+        double *fin = w + oF;
+        g.fin_nrmA = fin; g.fin_nrmB = fin + M; g.fin_maxA = fin + M + N; g.fin_maxB = fin + M + N + ntm;
+        g.fin_R = fin + M + N + ntm + ntn; g.fin_S = g.fin_R + (size_t)ntn * M;
         g.Rpre = pre ? Rpre : nullptr;
         g.Spre = pre ? Spre : nullptr;
         g.splits_r = (int)spR; g.splits_s = (int)spS;
@@ -463,14 +499,33 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
             CK(cudaMemsetAsync(Rpre, 0, (oS - oR + (size_t)spS * ntm * N) * sizeof(double), c.stream), "checksum zero");
             (void)nRS;
         }
+        if (pre) {
+            // per-row / per-column side data of the verification: partials summed once
+            FinArgs fa{};
+            fa.lineA = lineA; fa.lineB = lineB; fa.tmaxA = tmaxA; fa.tmaxB = tmaxB; fa.Rp = Rpre; fa.Sp = Spre;
+            fa.M = M; fa.N = N; fa.ntm = ntm; fa.ntn = ntn; fa.stride_r = g.stride_r; fa.stride_s = g.stride_s;
+            fa.kch = kch; fa.splits_r = (int)spR; fa.splits_s = (int)spS;
+            fa.nrmA = fin; fa.nrmB = fin + M; fa.maxA = fin + M + N; fa.maxB = fin + M + N + ntm;
+            fa.R = fin + M + N + ntm + ntn; fa.S = fa.R + (size_t)ntn * M;
+            const long long total = (long long)nF;
+            const unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 8 * 148);
+            side_finalize_kernel<<<blocks, 256, 0, c.stream>>>(fa);
+            c.launches++;
+            CK(cudaGetLastError(), "side_finalize_kernel launch");
+        }
         if (c.profiling) CK(cudaEventRecord(rec.e1, c.stream), "event");
         if (pre)
-            CK(launch_gemm<MODE_FT_PRE>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream), "gemm_kernel<FT> launch");
+            CK((pair ? launch_gemm<MODE_FT_PRE, 2>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream)
+                     : launch_gemm<MODE_FT_PRE, 4>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream)),
+               "gemm_kernel<FT> launch");
         else
-            CK(launch_gemm<MODE_FT_FUSED>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream), "gemm_kernel<FT> launch");
+            CK((launch_gemm<MODE_FT_FUSED, 4>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream)),
+               "gemm_kernel<FT> launch");
     } else {
         if (c.profiling) CK(cudaEventRecord(rec.e1, c.stream), "event");
-        CK(launch_gemm<MODE_NOFT>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream), "gemm_kernel launch");
+        CK((pair ? launch_gemm<MODE_NOFT, 2>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream)
+                 : launch_gemm<MODE_NOFT, 4>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream)),
+           "gemm_kernel launch");
     }
     if (c.profiling) {
         CK(cudaEventRecord(rec.e2, c.stream), "event");
@@ -645,6 +700,15 @@ int ftblas_set_checksum_mode(int mode) {
 }
 
 int ftblas_get_checksum_mode(void) { return ctx().checksum_mode; }
+
+int ftblas_set_tile_policy(int policy) {
+    if (policy != FTBLAS_TILES_AUTO && policy != FTBLAS_TILES_FULL && policy != FTBLAS_TILES_PAIR)
+        return arg_fail(1, "unknown tile policy");
+    ctx().tile_policy = policy;
+    return 0;
+}
+
+int ftblas_get_tile_policy(void) { return ctx().tile_policy; }
 
 int ftblas_set_stream(void *stream) {
     ctx().stream = static_cast<cudaStream_t>(stream);

@@ -133,6 +133,10 @@ struct GemmArgs {
     const double *Spre;    // FT_PRE: [splits_s][ntm][N], S[tm][j] = sum_k VA[tm][k] op(B)(k,j)
     int splits_r, splits_s;
     long long stride_r, stride_s;
+    // finalized side data (side_finalize_kernel): partials summed once, in fixed order
+    const double *fin_nrmA, *fin_nrmB;  // M, N  : ||op(A)(i,:)||_1, ||op(B)(:,j)||_1
+    const double *fin_maxA, *fin_maxB;  // ntm, ntn: tile maxima of the column / row |.| sums
+    const double *fin_R, *fin_S;        // FT_PRE: ntn x M, ntm x N (checksum GEMM results)
     // fault plan (CSR by tile, tile index = tn * ntm + tm)
     const int *plan_ptr;   // ntm*ntn + 1 or nullptr
     const long long *plan_i, *plan_j;
@@ -196,6 +200,21 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned b
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                      smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b))
                  : "memory");
+}
+// Distributed shared memory (cluster of 2): store to the same variable in CTA `rank` of the
+// cluster, and the cluster-wide barrier (release / acquire).
+__device__ __forceinline__ void st_cluster_f64(double *p, unsigned rank, double v) {
+    unsigned a;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+    asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster_s32(int *p, unsigned rank, int v) {
+    unsigned a;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+    asm volatile("st.shared::cluster.s32 [%0], %1;\n" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 // L2 prefetch of `bytes` (multiple of 16, 16-byte aligned source) -- no smem, no completion
 __device__ __forceinline__ void bulk_prefetch_l2(const void *src, unsigned bytes) {
@@ -441,13 +460,16 @@ constexpr int EPI_EL = 128 * LDT   /* tile */
 // fragments (DFMA), as the paper fuses them into its kernel.
 enum { MODE_NOFT = 0, MODE_FT_PRE = 1, MODE_FT_FUSED = 2 };
 
-template <int MODE>
+template <int MODE, int NWN = 4>
 struct SmemPlan {
-    static constexpr int STAGE_EL = 2 * TILE_EL;
-    static constexpr int PIPE_EL = STAGES * STAGE_EL + (MODE == MODE_FT_FUSED ? STAGES * 2 * BK : 0);
-    // every mode stages the C tile ([128][LDT]) in the drained pipeline bytes; FT adds the
+    static constexpr int BNT = 32 * NWN;
+    static constexpr int STAGE_EL = TILE_EL + BNT * BK;
+    static constexpr int NSTAGE = NWN == 4 ? STAGES : 2;  // pair CTAs: 2 per SM
+    static constexpr int PIPE_EL = NSTAGE * STAGE_EL + (MODE == MODE_FT_FUSED ? NSTAGE * 2 * BK : 0);
+    // every mode stages the C tile ([BNT][LDT]) in the drained pipeline bytes; FT adds the
     // reduction arrays
-    static constexpr int EPI = MODE != MODE_NOFT ? EPI_EL : 128 * LDT;
+    static constexpr int EPI_FT = BNT * LDT + NWN * 3 * 128 + 2 * 3 * BNT + 2 * 256 + 128 + 136;
+    static constexpr int EPI = MODE != MODE_NOFT ? EPI_FT : BNT * LDT;
     static constexpr int EL = EPI > PIPE_EL ? EPI : PIPE_EL;
     static constexpr int BYTES = 8 * EL + 1024;  // + alignment slack
 };
@@ -523,56 +545,77 @@ constexpr int LAUNCH_REGS = 168;
 constexpr int MMA_REGS = 224, PRODUCER_REGS = 56;  // 256x224 + 128x56 = 64512
 static_assert(NTHREADS * MMA_REGS + PRODUCER_THREADS * PRODUCER_REGS <= GEMM_THREADS * LAUNCH_REGS,
               "setmaxnreg budget exceeds the launch register allocation (would deadlock)");
+// Pair CTAs (2 per SM, 128 MMA + 128 producer threads): ptxas caps __launch_bounds__(256, 2) at
+// 128 registers, pool 256 x 128 = 32768 = 128 x 224 + 128 x 32.
+constexpr int PAIR_PRODUCER_REGS = 32;
+static_assert(128 * MMA_REGS + PRODUCER_THREADS * PAIR_PRODUCER_REGS <= 256 * 128, "pair setmaxnreg budget");
 
-template <bool KCA, bool KCB, bool TMA, int MODE>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+// NWN = warps along N.  NWN = 4: one CTA per 128 x 128 tile (8 MMA warps, 1 CTA / SM).
+// NWN = 2 ("pair"): one CTA per 128 x 64 half of a 128 x 128 verification tile (4 MMA warps,
+// 2 CTAs / SM, so one CTA's epilogue overlaps the other's mainloop); for FT the two halves
+// form a cluster of 2 and exchange their row partial sums and column-flag counts through
+// distributed shared memory, so verification, location and reports are those of the
+// 128 x 128 tile.
+template <bool KCA, bool KCB, bool TMA, int MODE, int NWN>
+__global__ void __launch_bounds__(64 * NWN + PRODUCER_THREADS, NWN == 2 ? 2 : 1)
     gemm_kernel(const __grid_constant__ GemmArgs g, const __grid_constant__ CUtensorMap tmA,
                 const __grid_constant__ CUtensorMap tmB) {
+    constexpr int NT = 64 * NWN;               // MMA threads
+    constexpr int BNT = 32 * NWN;              // CTA tile columns
+    constexpr bool FT = MODE != MODE_NOFT, FUSED = MODE == MODE_FT_FUSED;
+    constexpr bool PAIR = NWN == 2 && FT;      // cluster pair sharing one verification tile
+    static_assert(NWN == 4 || (NWN == 2 && !FUSED), "pair tiles: NOFT / FT_PRE only");
+    constexpr int PREG = NWN == 4 ? PRODUCER_REGS : PAIR_PRODUCER_REGS;
     extern __shared__ __align__(1024) double smem_raw[];
     __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES], norm_bar;
     // threshold norms of this tile (reading R4), reduced over the encode k-chunks by the
     // producer warpgroup while the MMA warps run the mainloop
-    __shared__ double nrm_row[BM], nrm_col[BN], nrm_max[2];
+    __shared__ double nrm_row[BM], nrm_col[BNT], nrm_max[2];
     // FT_PRE: this tile's slices of the checksum GEMM outputs R and S^T (loaded by the producer)
-    __shared__ double pre_r[MODE == MODE_FT_PRE ? BM : 1], pre_s[MODE == MODE_FT_PRE ? BN : 1];
-    constexpr bool FT = MODE != MODE_NOFT, FUSED = MODE == MODE_FT_FUSED;
+    __shared__ double pre_r[MODE == MODE_FT_PRE ? BM : 1], pre_s[MODE == MODE_FT_PRE ? BNT : 1];
+    // PAIR: row partial sums (out, C0, |C0|) and the column-flag count written by the peer CTA
+    __shared__ double peer_rows[PAIR ? 3 * BM : 1];
+    __shared__ int peer_nc;
     constexpr bool TMA_A = TMA, TMA_B = TMA;
     // 1024-byte aligned base, derived by indexing (keeps the pointer in the shared window so
     // the loads below use 32-bit shared addressing)
     double *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) / 8u;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp & 1, wn = warp >> 1;
-    const long long ntm = (g.M + BM - 1) / BM, ntn = (g.N + BN - 1) / BN;
+    const long long ntm = (g.M + BM - 1) / BM, ntn = (g.N + BN - 1) / BN;  // 128 x 128 tiles
     long long tm, tn;
-    tile_coords(blockIdx.x, ntm, ntn, tm, tn);
-    const long long m0 = tm * BM, n0 = tn * BN;
+    tile_coords(NWN == 4 ? blockIdx.x : blockIdx.x >> 1, ntm, ntn, tm, tn);
+    const int half = NWN == 4 ? 0 : (int)(blockIdx.x & 1);  // PAIR: also the cluster rank
+    const long long m0 = tm * BM, n0 = tn * BN + half * BNT;  // this CTA's columns [n0, n0 + BNT)
     const int ktiles = (g.alpha == 0.0) ? 0 : (int)((g.K + BK - 1) / BK);
+    using SP = SmemPlan<MODE, NWN>;
+    constexpr int NS = SP::NSTAGE;  // pipeline stages
 
-    auto sA = [&](int st) { return smem + st * SmemPlan<MODE>::STAGE_EL; };
-    auto sB = [&](int st) { return smem + st * SmemPlan<MODE>::STAGE_EL + TILE_EL; };
-    auto sW = [&](int st) { return smem + STAGES * SmemPlan<MODE>::STAGE_EL + st * 2 * BK; };
+    auto sA = [&](int st) { return smem + st * SP::STAGE_EL; };
+    auto sB = [&](int st) { return smem + st * SP::STAGE_EL + TILE_EL; };
+    auto sW = [&](int st) { return smem + NS * SP::STAGE_EL + st * 2 * BK; };
     auto sV = [&](int st) { return sW(st) + BK; };
 
     constexpr bool ALL_TMA = TMA_A && TMA_B;
     if (tid == 0) {
-        for (int s = 0; s < STAGES; s++) {
+        for (int s = 0; s < NS; s++) {
             // thread 0 of the producer arrives with expect_tx; cp.async fallback threads add
             // one arrival each when their copies land
             mbar_init(&full_bar[s], 1 + (ALL_TMA ? 0 : PRODUCER_THREADS));
-            mbar_init(&empty_bar[s], NTHREADS / 32);  // one arrival per MMA warp
+            mbar_init(&empty_bar[s], NT / 32);  // one arrival per MMA warp
         }
         mbar_init(&norm_bar, PRODUCER_THREADS - 32);  // producer warps 1..3
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
 
-    if (warp >= NTHREADS / 32) {
+    if (warp >= NT / 32) {
         // ------------------------------------------------------------ producer warpgroup
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
-        const int pt = tid - NTHREADS;
-        constexpr unsigned TX = (TMA_A ? TILE_EL * 8 : 0) + (TMA_B ? TILE_EL * 8 : 0) + (FUSED ? 2 * BK * 8 : 0);
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PREG));
+        const int pt = tid - NT;
+        constexpr unsigned TX = (TMA_A ? TILE_EL * 8 : 0) + (TMA_B ? BNT * BK * 8 : 0) + (FUSED ? 2 * BK * 8 : 0);
         auto produce = [&](int kt) {
-            const int st = kt % STAGES;
+            const int st = kt % NS;
             const long long k0 = (long long)kt * BK;
             if (pt == 0) {
                 mbar_arrive_expect_tx(&full_bar[st], TX);
@@ -582,31 +625,33 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 }
             }
             produce_tile<KCA, TMA_A>(sA(st), &tmA, &full_bar[st], g.A, g.lda, m0, k0, g.M, g.K, pt);
-            produce_tile<KCB, TMA_B>(sB(st), &tmB, &full_bar[st], g.B, g.ldb, n0, k0, g.N, g.K, pt);
+            produce_tile<KCB, TMA_B, BNT>(sB(st), &tmB, &full_bar[st], g.B, g.ldb, n0, k0, g.N, g.K, pt);
             if (!ALL_TMA) cp_async_mbar_arrive(&full_bar[st]);
         };
         if (FT && pt >= 32) {
             // Threshold norms (reading R4) and, for FT_PRE, the checksum-GEMM slices of this tile,
             // by producer warps 1..3 while thread 0 streams the operand stages: quantity q < 128 is
-            // row q, 128 <= q < 256 column q - 128, 256 / 257 the tile maxima of A / B.  Sums over
-            // the encode k-chunks / the k-splits in fixed order, loads issued in batches.
-            for (int q = pt - 32; q < 2 * 128 + 2; q += PRODUCER_THREADS - 32) {
+            // row q, 128 <= q < 128 + BNT column q - 128 of this CTA, then the tile maxima of A / B.
+            // Sums over the encode k-chunks / the k-splits in fixed order, loads issued in batches.
+            // With FT_PRE the per-row / per-column values were summed once by side_finalize_kernel
+            // and are only copied here (FP64 arithmetic beside the DMMA stream costs several
+            // times its share); the fused mode sums the partials itself.
+            for (int q = pt - 32; q < 128 + BNT + 2; q += PRODUCER_THREADS - 32) {
+                const bool fin = MODE == MODE_FT_PRE;
                 if (q < 128) {
                     const long long gi = m0 + q;
                     const bool ok = gi < g.M;
-                    nrm_row[q] = ok ? sum_strided(g.lineA + gi, g.M, g.kch) : 0.0;
-                    if (MODE == MODE_FT_PRE)
-                        pre_r[q] = ok ? sum_strided(g.Rpre + tn * g.M + gi, g.stride_r, g.splits_r) : 0.0;
-                } else if (q < 256) {
+                    nrm_row[q] = !ok ? 0.0 : fin ? g.fin_nrmA[gi] : sum_strided(g.lineA + gi, g.M, g.kch);
+                    if (MODE == MODE_FT_PRE) pre_r[q] = ok ? g.fin_R[tn * g.M + gi] : 0.0;
+                } else if (q < 128 + BNT) {
                     const long long gj = n0 + (q - 128);
                     const bool ok = gj < g.N;
-                    nrm_col[q - 128] = ok ? sum_strided(g.lineB + gj, g.N, g.kch) : 0.0;
-                    if (MODE == MODE_FT_PRE)
-                        pre_s[q - 128] = ok ? sum_strided(g.Spre + tm * g.N + gj, g.stride_s, g.splits_s) : 0.0;
-                } else if (q == 256) {
-                    nrm_max[0] = max_strided(g.tmaxA + tm, ntm, g.kch);
+                    nrm_col[q - 128] = !ok ? 0.0 : fin ? g.fin_nrmB[gj] : sum_strided(g.lineB + gj, g.N, g.kch);
+                    if (MODE == MODE_FT_PRE) pre_s[q - 128] = ok ? g.fin_S[tm * g.N + gj] : 0.0;
+                } else if (q == 128 + BNT) {
+                    nrm_max[0] = fin ? g.fin_maxA[tm] : max_strided(g.tmaxA + tm, ntm, g.kch);
                 } else {
-                    nrm_max[1] = max_strided(g.tmaxB + tn, ntn, g.kch);
+                    nrm_max[1] = fin ? g.fin_maxB[tn] : max_strided(g.tmaxB + tn, ntn, g.kch);
                 }
             }
             mbar_arrive(&norm_bar);
@@ -614,20 +659,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (ALL_TMA) {
             if (pt != 0) return;
             for (int kt = 0; kt < ktiles; kt++) {
-                if (kt == STAGES && g.beta != 0.0 && g.vecC) {
+                if (kt == NS && g.beta != 0.0 && g.vecC) {
                     // C0 of this tile -> L2 while the mainloop runs (the epilogue stages it into
                     // smem afterwards); after the first stages so it does not delay them
                     const unsigned bytes = (unsigned)(min((long long)BM, g.M - m0) * 8) & ~15u;
-                    const long long nv = min((long long)BN, g.N - n0);
+                    const long long nv = min((long long)BNT, g.N - n0);
                     if (bytes)
                         for (int c = 0; c < nv; c++) bulk_prefetch_l2(g.C + m0 + (n0 + c) * g.ldc, bytes);
                 }
-                if (kt >= STAGES) mbar_wait(&empty_bar[kt % STAGES], ((kt / STAGES) - 1) & 1);
+                if (kt >= NS) mbar_wait(&empty_bar[kt % NS], ((kt / NS) - 1) & 1);
                 produce(kt);
             }
         } else {
             for (int kt = 0; kt < ktiles; kt++) {
-                if (kt >= STAGES) mbar_wait(&empty_bar[kt % STAGES], ((kt / STAGES) - 1) & 1);
+                if (kt >= NS) mbar_wait(&empty_bar[kt % NS], ((kt / NS) - 1) & 1);
                 produce(kt);
             }
             cp_wait<0>();
@@ -635,6 +680,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         return;
     }
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(MMA_REGS));
+    auto bar_mma = [&]() { asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory"); };
 
     double acc[FM][FN][2];
 #pragma unroll
@@ -650,12 +696,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // fragments; the fragment is picked with warp-uniform selects (constant register indices).
     double rp[2] = {0.0, 0.0}, sp[2] = {0.0, 0.0};
     const FragAddr<KCA> fA(wm * WM, lane);
-    const FragAddr<KCB> fB(wn * WN, lane);
+    const FragAddr<KCB, BNT> fB(wn * WN, lane);
 
     // One pipeline stage; `st` is a compile-time constant (the k-tile loop is unrolled by
-    // STAGES), so every fragment address is a per-thread offset plus an immediate.
+    // NS), so every fragment address is a per-thread offset plus an immediate.
     auto consume = [&](const int st, const int kt) {
-        mbar_wait(&full_bar[st], (kt / STAGES) & 1);
+        mbar_wait(&full_bar[st], (kt / NS) & 1);
         const double *a_s = sA(st), *b_s = sB(st);
         const double *w_s = sW(st), *v_s = sV(st);
 #pragma unroll
@@ -684,9 +730,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[st]);
     };
-    for (int kt0 = 0; kt0 < ktiles; kt0 += STAGES) {
+    for (int kt0 = 0; kt0 < ktiles; kt0 += NS) {
 #pragma unroll
-        for (int st = 0; st < STAGES; st++)
+        for (int st = 0; st < NS; st++)
             if (kt0 + st < ktiles) consume(st, kt0 + st);
     }
     bar_mma();  // all MMA warps done with the pipeline smem (every issued copy was consumed)
@@ -701,11 +747,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // M x N), out = alpha acc + beta C0 is formed per fragment element, and the tile leaves
     // with coalesced column stores.
     double *tileS = smem;
-    const long long mvalid = min((long long)BM, g.M - m0), nvalid = min((long long)BN, g.N - n0);
+    // mvalid x nvalid: valid part of this CTA's block; tvalid: valid columns of the whole
+    // 128-wide verification tile (the row thresholds count all its columns)
+    const long long mvalid = min((long long)BM, g.M - m0), nvalid = max(0ll, min((long long)BNT, g.N - n0));
+    const long long tvalid = min((long long)BN, g.N - tn * BN);
     auto stage_c0 = [&]() {
         if (g.vecC) {
 #pragma unroll 8
-            for (int idx = tid; idx < BM * BN / 2; idx += NTHREADS) {
+            for (int idx = tid; idx < BM * BNT / 2; idx += NT) {
                 const int row = (idx & 63) * 2, col = idx >> 6;
                 const long long gi = m0 + row, gj = n0 + col;
                 const int nv = (gj < g.N) ? (int)min(2ll, max(0ll, g.M - gi)) : 0;
@@ -713,7 +762,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
         } else {
 #pragma unroll 8
-            for (int idx = tid; idx < BM * BN; idx += NTHREADS) {
+            for (int idx = tid; idx < BM * BNT; idx += NT) {
                 const int row = idx & 127, col = idx >> 7;
                 const long long gi = m0 + row, gj = n0 + col;
                 const bool ok = gi < g.M && gj < g.N;
@@ -742,7 +791,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     auto store_tile = [&]() {
         if (g.vecC) {
 #pragma unroll 8
-            for (int idx = tid; idx < BM * BN / 2; idx += NTHREADS) {
+            for (int idx = tid; idx < BM * BNT / 2; idx += NT) {
                 const int row = (idx & 63) * 2, col = idx >> 6;
                 if (col >= nvalid || row >= mvalid) continue;
                 double *dst = g.C + (m0 + row) + (n0 + col) * g.ldc;
@@ -750,7 +799,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 else                  *dst = tileS[row + col * LDT];
             }
         } else {
-            for (int idx = tid; idx < BM * BN; idx += NTHREADS) {
+            for (int idx = tid; idx < BM * BNT; idx += NT) {
                 const int row = idx & 127, col = idx >> 7;
                 if (row < mvalid && col < nvalid) g.C[(m0 + row) + (n0 + col) * g.ldc] = tileS[row + col * LDT];
             }
@@ -770,11 +819,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
 
     // -------------------------------------------------------------- FT epilogue
-    // partial row sums [wn][q][128] and column sums [wm][q][128], q = 0: out, 1: C0, 2: |C0|
-    double *red_r = tileS + 128 * LDT;       // 4 x 3 x 128
-    double *red_c = red_r + 4 * 3 * 128;     // 2 x 3 x 128
-    double *rsp = red_c + 2 * 3 * 128, *ssp = rsp + 256, *dres = ssp + 256;
-    int *flags = reinterpret_cast<int *>(dres + 128);  // [0] nrow, [1] ncol, [2..129] rows, [130..257] cols
+    // partial row sums [wn][q][128] and column sums [wm][q][BNT], q = 0: out, 1: C0, 2: |C0|
+    double *red_r = tileS + BNT * LDT;       // NWN x 3 x 128
+    double *red_c = red_r + NWN * 3 * 128;   // 2 x 3 x BNT
+    double *rsp = red_c + 2 * 3 * BNT, *ssp = rsp + 256, *dres = ssp + 256;
+    int *flags = reinterpret_cast<int *>(dres + 128);  // [0] nrow, [1] ncol, [2..129] rows, [130..] cols
 
     // checksum reference: FUSED -- combine the 4 k-lanes of the mainloop partials (fixed order),
     // one writer per row / column; FT_PRE -- the checksum-GEMM slices staged by the producer
@@ -870,7 +919,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     x += __shfl_xor_sync(0xffffffffu, x, 4);
                     x += __shfl_xor_sync(0xffffffffu, x, 8);
                     x += __shfl_xor_sync(0xffffffffu, x, 16);
-                    if (lane < 4) red_c[(wm * 3 + q) * 128 + col_of(b, e)] = x;
+                    if (lane < 4) red_c[(wm * 3 + q) * BNT + col_of(b, e)] = x;
                 }
         };
         col_red(cs, 0);
@@ -880,52 +929,84 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // verification: flag rows / columns beyond the round-off threshold
     const double aa = fabs(g.alpha), ab = fabs(g.beta);
     mbar_wait(&norm_bar, 0);  // producer-reduced norms are in nrm_row / nrm_col / nrm_max
-    if (tid < 128) {
-        const int r = tid;
-        if (r < mvalid) {
-            auto rsum = [&](int q) {
-                return ((red_r[(0 * 3 + q) * 128 + r] + red_r[(1 * 3 + q) * 128 + r]) + red_r[(2 * 3 + q) * 128 + r]) +
-                       red_r[(3 * 3 + q) * 128 + r];
-            };
-            const double sum = rsum(0);
-            const double rr2 = FUSED ? rsp[r] : pre_r[r];
-            const double c0s = beta0 ? 0.0 : rsum(1);
-            const double c0a = beta0 ? 0.0 : rsum(2);
-            const double ref = beta0 ? g.alpha * rr2 : fma(g.alpha, rr2, g.beta * c0s);
-            const double rowabs = nrm_row[r], bmax = nrm_max[1];
-            const double tau = 4.0 * U_ROUND * (double)(g.K + nvalid + 3) * (aa * rowabs * bmax + ab * c0a);
-            const double d = sum - ref;
-            dres[r] = d;
-            if (!(fabs(d) <= tau)) {
-                const int p = atomicAdd(&flags[0], 1);
-                flags[2 + p] = r;
+    // row sums of this CTA's columns (wn partials in fixed order); PAIR: exchanged with the
+    // peer half through distributed shared memory and added in half order (h0 + h1), so both
+    // CTAs hold the identical sums of the whole 128-wide tile
+    auto rsum_local = [&](int q, int r) {
+        double v = red_r[(0 * 3 + q) * 128 + r];
+#pragma unroll
+        for (int w = 1; w < NWN; w++) v += red_r[(w * 3 + q) * 128 + r];
+        return v;
+    };
+    if (PAIR) {
+        const unsigned peer = (unsigned)(half ^ 1);
+        for (int r = tid; r < BM; r += NT)
+#pragma unroll
+            for (int q = 0; q < 3; q++) {
+                const double v = rsum_local(q, r);
+                st_cluster_f64(&peer_rows[q * BM + r], peer, v);
             }
-        }
-    } else {
-        const int c = tid - 128;
-        if (c < nvalid) {
-            auto csum = [&](int q) { return red_c[(0 * 3 + q) * 128 + c] + red_c[(1 * 3 + q) * 128 + c]; };
-            const double sum = csum(0);
-            const double ss2 = FUSED ? ssp[c] : pre_s[c];
-            const double c0s = beta0 ? 0.0 : csum(1);
-            const double c0a = beta0 ? 0.0 : csum(2);
-            const double ref = beta0 ? g.alpha * ss2 : fma(g.alpha, ss2, g.beta * c0s);
-            const double colabs = nrm_col[c], amax = nrm_max[0];
-            const double tau = 4.0 * U_ROUND * (double)(g.K + mvalid + 3) * (aa * amax * colabs + ab * c0a);
-            const double d = sum - ref;
-            if (!(fabs(d) <= tau)) {
-                const int p = atomicAdd(&flags[1], 1);
-                flags[130 + p] = c;
+        cluster_sync();
+    }
+    auto rsum = [&](int q, int r) {
+        if (!PAIR) return rsum_local(q, r);
+        const double mine = rsum_local(q, r), theirs = peer_rows[q * BM + r];
+        return half == 0 ? mine + theirs : theirs + mine;
+    };
+    for (int qq = tid; qq < BM + BNT; qq += NT) {
+        if (qq < BM) {
+            const int r = qq;
+            if (r < mvalid) {
+                const double sum = rsum(0, r);
+                const double rr2 = FUSED ? rsp[r] : pre_r[r];
+                const double c0s = beta0 ? 0.0 : rsum(1, r);
+                const double c0a = beta0 ? 0.0 : rsum(2, r);
+                const double ref = beta0 ? g.alpha * rr2 : fma(g.alpha, rr2, g.beta * c0s);
+                const double rowabs = nrm_row[r], bmax = nrm_max[1];
+                const double tau = 4.0 * U_ROUND * (double)(g.K + tvalid + 3) * (aa * rowabs * bmax + ab * c0a);
+                const double d = sum - ref;
+                dres[r] = d;
+                if (!(fabs(d) <= tau)) {
+                    const int p = atomicAdd(&flags[0], 1);
+                    flags[2 + p] = r;
+                }
+            }
+        } else {
+            const int c = qq - BM;
+            if (c < nvalid) {
+                auto csum = [&](int q) { return red_c[(0 * 3 + q) * BNT + c] + red_c[(1 * 3 + q) * BNT + c]; };
+                const double sum = csum(0);
+                const double ss2 = FUSED ? ssp[c] : pre_s[c];
+                const double c0s = beta0 ? 0.0 : csum(1);
+                const double c0a = beta0 ? 0.0 : csum(2);
+                const double ref = beta0 ? g.alpha * ss2 : fma(g.alpha, ss2, g.beta * c0s);
+                const double colabs = nrm_col[c], amax = nrm_max[0];
+                const double tau = 4.0 * U_ROUND * (double)(g.K + mvalid + 3) * (aa * amax * colabs + ab * c0a);
+                const double d = sum - ref;
+                if (!(fabs(d) <= tau)) {
+                    const int p = atomicAdd(&flags[1], 1);
+                    flags[130 + p] = c;
+                }
             }
         }
     }
     bar_mma();
+    // nr: flagged rows of the verification tile (identical in both halves); nc: flagged columns
+    // of this CTA; nct: flagged columns of the whole tile (PAIR: + the peer's count)
     const int nr = flags[0], nc = flags[1];
-    if (nr != 0 || nc != 0) {
+    int nct = nc;
+    if (PAIR) {
+        if (tid == 0) st_cluster_s32(&peer_nc, (unsigned)(half ^ 1), nc);
+        cluster_sync();
+        nct = nc + peer_nc;
+    }
+    if (nr != 0 || nct != 0) {
         // ---------------------------------------------------------- locate + correct (rare)
         if (tid == 0) {
-            atomicAdd(&g.rep->tiles_flagged, 1ull);
-            atomicAdd(&g.rep->rows_flagged, (unsigned long long)nr);
+            if (half == 0) {  // once per verification tile
+                atomicAdd(&g.rep->tiles_flagged, 1ull);
+                atomicAdd(&g.rep->rows_flagged, (unsigned long long)nr);
+            }
             atomicAdd(&g.rep->cols_flagged, (unsigned long long)nc);
             for (int x = 1; x < nr; x++)
                 for (int y = x; y > 0 && flags[2 + y - 1] > flags[2 + y]; y--) {
@@ -937,9 +1018,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 }
         }
         bar_mma();
-        const bool single = (nr == 1 && nc == 1);  // Huang-Abraham location (line 540)
-        const long long ncr = nr ? nr : mvalid, ncc = nc ? nc : nvalid;
-        for (long long q = warp; q < ncr * ncc; q += NTHREADS / 32) {
+        const bool single = (nr == 1 && nct == 1);  // Huang-Abraham location (line 540)
+        // candidates: (flagged rows, or all rows) x (this CTA's flagged columns, or all its
+        // columns when no column of the tile is flagged); none when only the peer has flags
+        const long long ncr = nr ? nr : mvalid, ncc = nct ? nc : nvalid;
+        for (long long q = warp; q < ncr * ncc; q += NT / 32) {
             const int r = nr ? flags[2 + (int)(q % ncr)] : (int)(q % ncr);
             const int c = nc ? flags[130 + (int)(q / ncr)] : (int)(q / ncr);
             const long long gi = m0 + r, gj = n0 + c;
@@ -954,7 +1037,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 const unsigned long long p = atomicAdd(&g.rep->count, 1ull);
                 if ((long long)p < g.rep_cap) {
                     Correction cr;
-                    cr.tile_m = tm + g.off_i / BM; cr.tile_n = tn + g.off_j / BN;
+                    cr.tile_m = tm + g.off_i / BM; cr.tile_n = tn + g.off_j / BN;  // the 128 x 128 tile
                     cr.i = gi + g.off_i; cr.j = gj + g.off_j;
                     cr.residual = dres[r];
                     cr.kind = single ? 1 : 2; cr.pad = 0;
@@ -968,6 +1051,36 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     store_tile();
 }
 
+
+
+// ------------------------------------------------------------------ side-data finalize
+// FT_PRE: sums the per-k-chunk norm partials of encode_kernel and the k-split partials of the
+// checksum GEMMs in fixed (index) order into one value per row / column (and the tile maxima),
+// so the GEMM kernel only copies them (grid-stride, HBM-bound, one read of every partial).
+struct FinArgs {
+    const double *lineA, *lineB, *tmaxA, *tmaxB, *Rp, *Sp;
+    long long M, N, ntm, ntn, stride_r, stride_s;
+    int kch, splits_r, splits_s;
+    double *nrmA, *nrmB, *maxA, *maxB, *R, *S;
+};
+__global__ void __launch_bounds__(256) side_finalize_kernel(FinArgs f) {
+    const long long nA = f.M, nB = f.N, nmA = f.ntm, nmB = f.ntn, nR = f.ntn * f.M, nS = f.ntm * f.N;
+    const long long total = nA + nB + nmA + nmB + nR + nS;
+    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (long long)gridDim.x * blockDim.x) {
+        long long y = x;
+        if (y < nA) { f.nrmA[y] = sum_strided(f.lineA + y, f.M, f.kch); continue; }
+        y -= nA;
+        if (y < nB) { f.nrmB[y] = sum_strided(f.lineB + y, f.N, f.kch); continue; }
+        y -= nB;
+        if (y < nmA) { f.maxA[y] = max_strided(f.tmaxA + y, f.ntm, f.kch); continue; }
+        y -= nmA;
+        if (y < nmB) { f.maxB[y] = max_strided(f.tmaxB + y, f.ntn, f.kch); continue; }
+        y -= nmB;
+        if (y < nR) { f.R[y] = sum_strided(f.Rp + y, f.stride_r, f.splits_r); continue; }
+        y -= nR;
+        f.S[y] = sum_strided(f.Sp + y, f.stride_s, f.splits_s);
+    }
+}
 
 // ------------------------------------------------------------------ checksum GEMM kernel
 // The checksum GEMMs of MODE_FT_PRE (the border of C^f = A^c B^r):

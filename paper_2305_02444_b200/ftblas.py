@@ -70,6 +70,10 @@ def _load():
     L.ftblas_dgemm_ex.restype = ct.c_int
     L.ftblas_report_reset.argtypes = []
     L.ftblas_report_reset.restype = ct.c_int
+    L.ftblas_set_tile_policy.argtypes = [ct.c_int]
+    L.ftblas_set_tile_policy.restype = ct.c_int
+    L.ftblas_get_tile_policy.argtypes = []
+    L.ftblas_get_tile_policy.restype = ct.c_int
     L.ftblas_set_checksum_mode.argtypes = [ct.c_int]
     L.ftblas_set_checksum_mode.restype = ct.c_int
     L.ftblas_get_checksum_mode.argtypes = []
@@ -84,7 +88,10 @@ EXPORTS = ("ftblas_dgemm", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_rep
            "ftblas_set_fault_plan", "ftblas_set_stream", "ftblas_launch_count",
            "ftblas_tile_shape", "ftblas_last_error", "ftblas_release", "ftblas_profile",
            "ftblas_profile_read", "ftblas_set_checksum_mode", "ftblas_get_checksum_mode",
-           "ftblas_dgemm_ex", "ftblas_report_reset")
+           "ftblas_dgemm_ex", "ftblas_report_reset", "ftblas_set_tile_policy",
+           "ftblas_get_tile_policy")
+
+TILES = {"auto": 0, "full": 1, "pair": 2}  # FTBLAS_TILES_*
 
 REPORT_APPEND = 1  # FTBLAS_REPORT_APPEND
 REUSE_A_ENCODE = 2  # FTBLAS_REUSE_A_ENCODE
@@ -200,6 +207,15 @@ def ftblas_clear_fault_plan():
 def ftblas_set_checksum_mode(mode):
     """mode: CHECKSUM_GEMM / CHECKSUM_FUSED or the names 'gemm' / 'fused'."""
     _check(lib.ftblas_set_checksum_mode(CHECKSUM_MODES.get(mode, mode)))
+
+
+def ftblas_set_tile_policy(policy):
+    """policy: 'auto' | 'full' | 'pair' or the FTBLAS_TILES_* value."""
+    _check(lib.ftblas_set_tile_policy(TILES.get(policy, policy)))
+
+
+def ftblas_get_tile_policy() -> int:
+    return lib.ftblas_get_tile_policy()
 
 
 def ftblas_get_checksum_mode() -> int:

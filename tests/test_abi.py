@@ -115,3 +115,14 @@ def test_ex_argument_errors(lib, roff, coff, flags, code):
     rc = lib.lib.ftblas_dgemm_ex(b"N", b"N", 4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, roff, coff,
                                  flags, None)
     assert rc == code
+
+
+def test_tile_policy_api(lib):
+    """ftblas_set_tile_policy accepts the three policies of the header (host state only)."""
+    assert lib.ftblas_get_tile_policy() == lib.TILES["auto"]
+    for name in ("full", "pair", "auto"):
+        lib.ftblas_set_tile_policy(name)
+        assert lib.ftblas_get_tile_policy() == lib.TILES[name]
+    with pytest.raises(lib.FtblasError):
+        lib.ftblas_set_tile_policy(9)
+    lib.ftblas_set_tile_policy("auto")

@@ -16,22 +16,26 @@ from tests._util import from_dev, gemm_bound, report_key, to_dev
 pytestmark = pytest.mark.gpu
 
 
-def _lib(mode):
+def _lib(mode, tiles="auto"):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2305_02444_b200 import ftblas
     ftblas.ftblas_set_stream(None)
     ftblas.ftblas_set_checksum_mode(mode)
+    ftblas.ftblas_set_tile_policy(tiles)
     return ftblas
 
 
-@pytest.fixture(params=["gemm", "fused"])
+@pytest.fixture(params=[("gemm", "pair"), ("gemm", "full"), ("fused", "full")],
+                ids=["gemm-pair", "gemm-full", "fused-full"])
 def ft(request):
-    """The library in each checksum mode (checksum GEMMs / fused mainloop checksums)."""
-    lib = _lib(request.param)
+    """The library in each checksum mode (checksum GEMMs / fused mainloop checksums) and CTA
+    tiling (128 x 64 cluster-pair halves / 128 x 128 tiles)."""
+    lib = _lib(*request.param)
     yield lib
     lib.ftblas_set_checksum_mode("gemm")
+    lib.ftblas_set_tile_policy("auto")
 
 
 @pytest.fixture

@@ -8,12 +8,22 @@ libs = sys.argv[1:] or sorted(glob.glob(os.path.join(os.path.dirname(__file__), 
 P, I, D = ct.c_void_p, ct.c_int64, ct.c_double
 common = [ct.c_char, ct.c_char, I, I, I, D, P, I, P, I, D, P, I]
 Ls = []
-for path in libs:
-    L = ct.CDLL(path)
+import shutil, tempfile
+for spec in libs:
+    path, _, policy = spec.partition(":")
+    if policy:  # a private copy: ctypes would share one handle (and its state) per path
+        tmp = os.path.join(tempfile.mkdtemp(), policy + "_" + os.path.basename(path))
+        shutil.copy(path, tmp)
+        L = ct.CDLL(tmp)
+    else:
+        L = ct.CDLL(path)
     L.ftblas_dgemm.argtypes = common + [P]; L.ftblas_dgemm_noft.argtypes = common
     L.ftblas_set_stream.argtypes = [P]
     L.ftblas_set_stream(ct.c_void_p(torch.cuda.current_stream().cuda_stream))
-    Ls.append((os.path.basename(path), L))
+    if policy:
+        L.ftblas_set_tile_policy.argtypes = [ct.c_int]
+        L.ftblas_set_tile_policy({"auto": 0, "full": 1, "pair": 2}[policy])
+    Ls.append((os.path.basename(path) + (":" + policy if policy else ""), L))
 for w in syn.CONFIGS[:4]:
     M, N, K = w.M, w.N, w.K
     lda = M if w.transA == "N" else K; ldb = K if w.transB == "N" else N
@@ -32,5 +42,5 @@ for w in syn.CONFIGS[:4]:
             e1.record(); torch.cuda.synchronize()
             res.append(e0.elapsed_time(e1) / reps)
         fl = 2.0 * M * N * K
-        print(f"{w.name:22s} {name:16s} noft {res[0]:8.3f} ms {fl/res[0]/1e9:6.2f} TF | ft {res[1]:8.3f} ms {fl/res[1]/1e9:6.2f} TF ovh {100*(res[1]/res[0]-1):5.2f}%", flush=True)
+        print(f"{w.name:22s} {name:20s} noft {res[0]:8.3f} ms {fl/res[0]/1e9:6.2f} TF | ft {res[1]:8.3f} ms {fl/res[1]/1e9:6.2f} TF ovh {100*(res[1]/res[0]-1):5.2f}%", flush=True)
     del A, B, C
