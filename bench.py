@@ -267,7 +267,7 @@ def main():
 
     # N > 1: op(B) is broadcast in column chunks of whole tiles, the GEMM of chunk c overlapping
     # the broadcast of chunks > c (shard.sharded_dgemm); N = 1: one call, no exchange.
-    chunks = 8 if (world > 1 and w.transB == "N") else 1
+    chunks = shard.broadcast_chunks(m, w.N) if (world > 1 and w.transB == "N") else 1
 
     def step(gemm, broadcast):
         # C := alpha AB + beta C accumulates into C; the value drifts but the work is identical

@@ -69,6 +69,15 @@ def chunk_bounds(N: int, chunks: int, align: int = TILE_N) -> list:
     return out
 
 
+def broadcast_chunks(m: int, N: int, sms: int = 148, waves: int = 7, max_chunks: int = 8) -> int:
+    """Column chunks for the overlapped op(B) broadcast of a rank with m rows.  The GEMM of a
+    chunk is one launch, so each chunk should hold about ``waves`` full waves of 128 x 128 tiles
+    (a chunk of 1.7 waves costs 13 % in the last partial wave); within that, more chunks hide
+    more of the broadcast."""
+    tiles = -(-m // TILE_M) * -(-N // TILE_N)
+    return max(1, min(max_chunks, -(-N // TILE_N), round(tiles / (waves * sms))))
+
+
 def sharded_dgemm(gemm, transA, transB, M, N, K, alpha, A_shard, lda, B, ldb, beta, C_shard, ldc,
                   *, rank: int, world: int, src: int = 0, group=None, broadcast: bool = True,
                   chunks: int = 1):

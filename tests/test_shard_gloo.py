@@ -119,3 +119,12 @@ def test_chunk_bounds_whole_tiles():
             assert b[0][0] == 0 and b[-1][1] == N
             assert all(c0 % 128 == 0 and c0 < c1 for c0, c1 in b)
             assert all(p[1] == q[0] for p, q in zip(b, b[1:]))
+
+
+def test_broadcast_chunks_keep_whole_waves():
+    # c3 at 8 / 4 / 2 GPUs: 2048 / 4096 / 8192 tiles per rank -> chunks of ~1024 tiles (7 waves)
+    assert shard.broadcast_chunks(2048, 16384) == 2
+    assert shard.broadcast_chunks(4096, 16384) == 4
+    assert shard.broadcast_chunks(8192, 16384) == 8
+    assert shard.broadcast_chunks(128, 300) == 1
+    assert shard.broadcast_chunks(4096, 32768) == 8
