@@ -147,15 +147,18 @@ def test_injected_flips_reports_bit_exact(ft, tA, tB):
 
 
 def test_multiple_errors_in_one_tile(ft):
-    """Two flips in one tile (distinct rows/cols) and two in one row: candidate path (kind 2)."""
+    """Two flips in one tile (distinct rows/cols) and two in one row: candidate path (kind 2).
+    Tiles (1,1) and (0,1) put the two columns in different 64-column halves (the two CTAs of a
+    pair tile): same row, and different rows."""
     w = syn.Workload("t", 256, 256, 64, "N", "N", 1.0, 0.0, "uniform", False, seed=3)
     d = syn.make_inputs(w)
-    plan = (np.array([3, 40, 200, 200], np.int64), np.array([10, 55, 130, 250], np.int64),
-            np.array([50, 58, 45, 61], np.int32))
+    plan = (np.array([3, 40, 200, 200, 5, 70], np.int64), np.array([10, 55, 130, 250, 140, 230], np.int64),
+            np.array([50, 58, 45, 61, 52, 44], np.int32))
     C_gpu, rep = run_gpu(ft, w, d, plan=plan)
     C_ref, orep, st = run_oracle(w, d, plan)
     assert report_key(rep.entries()) == report_key(orep)
-    assert sorted((e["i"], e["j"]) for e in rep.entries()) == [(3, 10), (40, 55), (200, 130), (200, 250)]
+    assert sorted((e["i"], e["j"]) for e in rep.entries()) == [(3, 10), (5, 140), (40, 55), (70, 230),
+                                                               (200, 130), (200, 250)]
     assert_close(w, d, C_gpu, C_ref)
 
 
