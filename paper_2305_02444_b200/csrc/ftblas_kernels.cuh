@@ -501,7 +501,7 @@ __device__ __forceinline__ double max_strided(const double *p, long long stride,
 
 // Tile rasterization: groups of GROUP_M tile-rows, column-major inside a group, so the
 // CTAs resident at one time share a few A row panels and B column panels in L2.
-constexpr int GROUP_M = 16;
+constexpr int GROUP_M = 8;
 __device__ __forceinline__ void tile_coords(long long x, long long ntm, long long ntn, long long &tm, long long &tn) {
     const long long gsz = (long long)GROUP_M * ntn;
     const long long grp = x / gsz, first = grp * GROUP_M;
