@@ -350,3 +350,29 @@ def test_config4_32768x16384(ftd):
     """configs[4] is quoted for an 8-GPU row-block shard; each shard runs the single-GPU call,
     so the whole problem on one GPU (17 GB of operands) checks the same kernels at full size."""
     check_full_config(ftd, syn.CONFIGS[4], oracle_tiles=4)
+
+
+def test_zero_fault_transparency_and_no_false_positives(ft):
+    """Fault-free ftblas_dgemm is bitwise identical to ftblas_dgemm_noft (the checksum work is
+    additive: same DMMA sequence and epilogue formula) and flags nothing, over random shapes
+    (1..400 x 1..400 x 1..300, all transposes, random alpha / beta) -- the SPEC's
+    zero-fault-transparency and checksum-identity criteria at desk scale."""
+    import torch
+    rng = np.random.default_rng(2024)
+    for trial in range(24):
+        M, N = (int(x) for x in rng.integers(1, 401, 2))
+        K = int(rng.integers(1, 301))
+        tA, tB = ("N", "T")[int(rng.integers(2))], ("N", "T")[int(rng.integers(2))]
+        alpha = float(rng.choice([1.0, -1.0, 0.5, 2.5]))
+        beta = float(rng.choice([0.0, 1.0, -0.5]))
+        w = syn.Workload("zf", M, N, K, tA, tB, alpha, beta, "normal", True, seed=100 + trial)
+        d = syn.make_inputs(w)
+        A_t, pA = to_dev(d["A"]); B_t, pB = to_dev(d["B"])
+        C1_t, pC1 = to_dev(d["C"]); C2_t, pC2 = to_dev(d["C"])
+        ft.ftblas_clear_fault_plan()
+        rep = ft.Report(16)
+        ft.ftblas_dgemm(tA, tB, M, N, K, alpha, pA, d["lda"], pB, d["ldb"], beta, pC1, d["ldc"], rep)
+        ft.ftblas_dgemm_noft(tA, tB, M, N, K, alpha, pA, d["lda"], pB, d["ldb"], beta, pC2, d["ldc"])
+        torch.cuda.synchronize()
+        assert rep.count == 0 and rep.tiles_flagged == 0, (M, N, K, tA, tB)
+        assert torch.equal(C1_t, C2_t), (M, N, K, tA, tB, alpha, beta)
