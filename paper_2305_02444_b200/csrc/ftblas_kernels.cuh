@@ -15,8 +15,11 @@
 //                   (lines 517, 540, 521) before the store.  FT=false is the non-FT
 //                   baseline (same tiles/mainloop).
 //
-// CTA: 8 MMA warps in a 2 (M) x 4 (N) grid, warp tile 64 x 32 = 8 x 4 DMMA fragments of
-// 8x8, CTA tile 128 x 128, BK = 32, plus one producer warpgroup.  See DESIGN.md section 5.
+// CTA: MMA warps in a 2 (M) x NWN (N) grid, warp tile 64 x 32 = 8 x 4 DMMA fragments of 8x8,
+// BK = 32, plus one producer warpgroup.  NWN = 4: 128 x 128 CTA tile, one CTA per SM, 3-stage
+// ring.  NWN = 2 ("pair"): 128 x 64 CTA tile, two CTAs per SM, 2-stage ring; in FT mode the
+// two halves of a 128 x 128 verification tile are a cluster exchanging row sums through DSMEM.
+//   side_finalize_kernel / cksum_kernel: see their sections.  DESIGN.md section 5.
 #pragma once
 #include <cstdint>
 #include <cuda.h>
@@ -442,12 +445,7 @@ __global__ void __launch_bounds__(NTHREADS) encode_kernel(EncodeArgs a) {
 
 // ------------------------------------------------------------------ GEMM kernel
 constexpr int LDT = 130;  // epilogue tile leading dimension (conflict-free fragment stores)
-constexpr int EPI_EL = 128 * LDT   /* tile */
-                     + 12 * 128    /* red_r[4][3][128] */
-                     + 6 * 128     /* red_c[2][3][128] */
-                     + 2 * 256     /* rsp[128], ssp[128] (+ spare) */
-                     + 128         /* row residuals */
-                     + 136;        /* flags (int) */
+        /* flags (int) */
 
 // Dynamic smem: [STAGES][A tile | B tile] (1024-byte aligned boxes for the 128-byte swizzle),
 // then [STAGES][w_J slice | v_I slice] (FT checksum vectors, BK each).  The FT epilogue
