@@ -499,8 +499,9 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
             CK(cudaMemsetAsync(Rpre, 0, (oS - oR + (size_t)spS * ntm * N) * sizeof(double), c.stream), "checksum zero");
             (void)nRS;
         }
-        if (pre) {
-            // per-row / per-column side data of the verification: partials summed once
+        if (pre && pair) {
+            // per-row / per-column side data of the verification: partials summed once (the
+            // pair-tile producers copy them; 128 x 128 tiles sum the partials in the producer)
             FinArgs fa{};
             fa.lineA = lineA; fa.lineB = lineB; fa.tmaxA = tmaxA; fa.tmaxB = tmaxB; fa.Rp = Rpre; fa.Sp = Spre;
             fa.M = M; fa.N = N; fa.ntm = ntm; fa.ntn = ntn; fa.stride_r = g.stride_r; fa.stride_s = g.stride_s;

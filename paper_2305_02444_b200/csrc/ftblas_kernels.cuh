@@ -635,17 +635,23 @@ __global__ void __launch_bounds__(64 * NWN + PRODUCER_THREADS, NWN == 2 ? 2 : 1)
             // and are only copied here (FP64 arithmetic beside the DMMA stream costs several
             // times its share); the fused mode sums the partials itself.
             for (int q = pt - 32; q < 128 + BNT + 2; q += PRODUCER_THREADS - 32) {
-                const bool fin = MODE == MODE_FT_PRE;
+                // pair tiles (producer warps at 32 registers) copy finalized sums; 128 x 128 tiles
+                // sum the partials themselves and skip the finalize launch
+                constexpr bool fin = MODE == MODE_FT_PRE && NWN == 2;
                 if (q < 128) {
                     const long long gi = m0 + q;
                     const bool ok = gi < g.M;
                     nrm_row[q] = !ok ? 0.0 : fin ? g.fin_nrmA[gi] : sum_strided(g.lineA + gi, g.M, g.kch);
-                    if (MODE == MODE_FT_PRE) pre_r[q] = ok ? g.fin_R[tn * g.M + gi] : 0.0;
+                    if (MODE == MODE_FT_PRE)
+                        pre_r[q] = !ok ? 0.0 : fin ? g.fin_R[tn * g.M + gi]
+                                                   : sum_strided(g.Rpre + tn * g.M + gi, g.stride_r, g.splits_r);
                 } else if (q < 128 + BNT) {
                     const long long gj = n0 + (q - 128);
                     const bool ok = gj < g.N;
                     nrm_col[q - 128] = !ok ? 0.0 : fin ? g.fin_nrmB[gj] : sum_strided(g.lineB + gj, g.N, g.kch);
-                    if (MODE == MODE_FT_PRE) pre_s[q - 128] = ok ? g.fin_S[tm * g.N + gj] : 0.0;
+                    if (MODE == MODE_FT_PRE)
+                        pre_s[q - 128] = !ok ? 0.0 : fin ? g.fin_S[tm * g.N + gj]
+                                                         : sum_strided(g.Spre + tm * g.N + gj, g.stride_s, g.splits_s);
                 } else if (q == 128 + BNT) {
                     nrm_max[0] = fin ? g.fin_maxA[tm] : max_strided(g.tmaxA + tm, ntm, g.kch);
                 } else {
