@@ -267,7 +267,7 @@ def main():
 
     # N > 1: op(B) is broadcast in column chunks of whole tiles, the GEMM of chunk c overlapping
     # the broadcast of chunks > c (shard.sharded_dgemm); N = 1: one call, no exchange.
-    chunks = shard.broadcast_chunks(m, w.N) if (world > 1 and w.transB == "N") else 1
+    chunks = shard.broadcast_chunk_bounds(m, w.N) if (world > 1 and w.transB == "N") else 1
 
     def step(gemm, broadcast):
         # C := alpha AB + beta C accumulates into C; the value drifts but the work is identical
@@ -394,8 +394,10 @@ def main():
                        "injected_flips": w.n_flips, "flip_bits": [syn.BIT_LO, syn.BIT_HI],
                        "verification_tile": [syn.TILE_M, syn.TILE_N],
                        "parallelism": f"row-block x{world}" + (
-                           (f", op(B) {args.backend.upper()} broadcast per step in {chunks} column chunks overlapped with the GEMM"
-                            if chunks > 1 else f", op(B) {args.backend.upper()} broadcast per step") if world > 1 else ""),
+                           (f", op(B) {args.backend.upper()} broadcast per step in {len(chunks)} column chunks "
+                            f"{[c1 - c0 for c0, c1 in chunks]} overlapped with the GEMM"
+                            if isinstance(chunks, list) else f", op(B) {args.backend.upper()} broadcast per step")
+                           if world > 1 else ""),
                        "l2": "no flush: operands (%.1f GiB) >> 126 MB L2" % ((d["A"].nbytes + d["B"].nbytes + d["C"].nbytes) / 2**30)},
             "fp64_peak_tflops": FP64_PEAK_TFLOPS,
             "pct_fp64_peak": 100.0 * value / (FP64_PEAK_TFLOPS * world),

@@ -69,18 +69,28 @@ def chunk_bounds(N: int, chunks: int, align: int = TILE_N) -> list:
     return out
 
 
-def broadcast_chunks(m: int, N: int, sms: int = 148, waves: int = 7, max_chunks: int = 8) -> int:
-    """Column chunks for the overlapped op(B) broadcast of a rank with m rows.  The GEMM of a
-    chunk is one launch, so each chunk should hold about ``waves`` full waves of 128 x 128 tiles
-    (a chunk of 1.7 waves costs 13 % in the last partial wave); within that, more chunks hide
-    more of the broadcast."""
-    tiles = -(-m // TILE_M) * -(-N // TILE_N)
-    return max(1, min(max_chunks, -(-N // TILE_N), round(tiles / (waves * sms))))
+def broadcast_chunk_bounds(m: int, N: int, sms: int = 148, waves=(1, 2, 4)) -> list:
+    """Column blocks [c0, c1) of whole tiles for the overlapped op(B) broadcast of a rank with m
+    rows: a geometric schedule of about 1, 2, 4 waves of 128 x 128 tiles, then the rest.  Only
+    the first (one-wave) block's broadcast is exposed; each later block has the previous
+    block's GEMM to arrive in, and every block is (close to) whole waves, since each block is
+    one GEMM launch and a partial last wave idles SMs."""
+    rows = -(-m // TILE_M)
+    cols = -(-N // TILE_N)
+    out, c = [], 0
+    for w in waves:
+        take = max(1, (w * sms) // rows)
+        if c + take >= cols:
+            break
+        out.append((c * TILE_N, (c + take) * TILE_N))
+        c += take
+    out.append((c * TILE_N, N))
+    return out
 
 
 def sharded_dgemm(gemm, transA, transB, M, N, K, alpha, A_shard, lda, B, ldb, beta, C_shard, ldc,
                   *, rank: int, world: int, src: int = 0, group=None, broadcast: bool = True,
-                  chunks: int = 1):
+                  chunks=1):
     """One sharded step on this rank.
 
     ``gemm(transA, transB, m, n, K, alpha, A, lda, B, ldb, beta, C, ldc, col_offset, append)``
@@ -91,7 +101,8 @@ def sharded_dgemm(gemm, transA, transB, M, N, K, alpha, A_shard, lda, B, ldb, be
     C_shard its (r1-r0) x N rows of C as flat column-major storage (ld ``ldc``), B the flat
     column-major storage of B (ld ``ldb``).
 
-    The exchange of the step is the broadcast of op(B) from ``src``.  With ``chunks > 1`` and
+    The exchange of the step is the broadcast of op(B) from ``src``.  With ``chunks`` > 1 (a
+    count, or an explicit list of column blocks such as ``broadcast_chunk_bounds``) and
     transB = 'N' (column blocks of op(B) are contiguous in B) it is split into column blocks
     of whole tiles, all posted asynchronously on the communication stream; the GEMM of block
     c waits only for block c, so the broadcast of the later blocks overlaps the DMMA work of
@@ -100,9 +111,9 @@ def sharded_dgemm(gemm, transA, transB, M, N, K, alpha, A_shard, lda, B, ldb, be
     r0, r1 = shard_rows(M, world, rank)
     m = r1 - r0
     multi = broadcast and world > 1
-    if multi and chunks > 1 and transB in ("N", "n"):
+    bounds = chunks if isinstance(chunks, (list, tuple)) else chunk_bounds(N, chunks)
+    if multi and len(bounds) > 1 and transB in ("N", "n"):
         import torch.distributed as dist
-        bounds = chunk_bounds(N, chunks)
         works = [dist.broadcast(B[c0 * ldb: c1 * ldb], src=src, group=group, async_op=True)
                  for (c0, c1) in bounds]
         for q, (c0, c1) in enumerate(bounds):

@@ -121,10 +121,16 @@ def test_chunk_bounds_whole_tiles():
             assert all(p[1] == q[0] for p, q in zip(b, b[1:]))
 
 
-def test_broadcast_chunks_keep_whole_waves():
-    # c3 at 8 / 4 / 2 GPUs: 2048 / 4096 / 8192 tiles per rank -> chunks of ~1024 tiles (7 waves)
-    assert shard.broadcast_chunks(2048, 16384) == 2
-    assert shard.broadcast_chunks(4096, 16384) == 4
-    assert shard.broadcast_chunks(8192, 16384) == 8
-    assert shard.broadcast_chunks(128, 300) == 1
-    assert shard.broadcast_chunks(4096, 32768) == 8
+def test_broadcast_chunk_bounds_geometric_whole_waves():
+    import math
+    for m, N in [(2048, 16384), (4096, 16384), (8192, 16384), (4096, 32768), (300, 300), (16384, 256)]:
+        b = shard.broadcast_chunk_bounds(m, N)
+        assert b[0][0] == 0 and b[-1][1] == N
+        assert all(c0 % 128 == 0 and c0 < c1 for c0, c1 in b)
+        assert all(p[1] == q[0] for p, q in zip(b, b[1:]))
+        rows = -(-m // 128)
+        waves = [math.ceil(rows * -(-(c1 - c0) // 128) / 148) for c0, c1 in b]
+        ideal = rows * -(-N // 128) / 148
+        assert sum(waves) <= math.ceil(ideal) + 1, (m, N, b, waves, ideal)
+    # c3 at 8 GPUs: 9 / 18 / 37 tile-columns (1, 2, 4 waves), then the rest
+    assert [(c1 - c0) // 128 for c0, c1 in shard.broadcast_chunk_bounds(2048, 16384)] == [9, 18, 37, 64]
