@@ -253,7 +253,7 @@ constexpr int PRODUCER_THREADS = 128;  // one warpgroup; registers go to the MMA
 // TMA=false (operand pointer not 16-byte aligned or odd ld, where a tensor map cannot be
 // built): every producer thread copies 8-byte elements with cp.async, zero-fill outside
 // [0,MNd) x [0,Kd).
-template <bool KC, bool TMA, int ROWS = 128>
+template <bool KC, bool TMA, int ROWS = 128, int NTP = PRODUCER_THREADS>
 __device__ __forceinline__ void produce_tile(double *s, const CUtensorMap *map, unsigned long long *bar,
                                              const double *X, long long ld, long long mn0, long long k0,
                                              long long MNd, long long Kd, int pt) {
@@ -269,7 +269,7 @@ __device__ __forceinline__ void produce_tile(double *s, const CUtensorMap *map, 
         }
     } else {
 #pragma unroll 4
-        for (int c = pt; c < ROWS * BK; c += PRODUCER_THREADS) {
+        for (int c = pt; c < ROWS * BK; c += NTP) {
             int mn, k;
             if (KC) { mn = c / BK; k = c % BK; }
             else    { k = c / ROWS; mn = c % ROWS; }
@@ -458,6 +458,22 @@ constexpr int LDT = 130;  // epilogue tile leading dimension (conflict-free frag
 // fragments (DFMA), as the paper fuses them into its kernel.
 enum { MODE_NOFT = 0, MODE_FT_PRE = 1, MODE_FT_FUSED = 2 };
 
+// Warp layout of a gemm_kernel CTA (128 x 32 NWN tile).  Both layouts have 8 MMA warps, two
+// per SM sub-partition, which is what keeps the DMMA pipe fed (tools/dmma_mainloop.cu: a
+// 128 x 64 CTA of 4 warps reaches 32.5 TFLOP/s alone, of 8 warps 32 x 32 36.9).
+//   NWN = 4: 2 (M) x 4 (N) warps of 64 x 32, producer warpgroup (setmaxnreg 224 / 56).
+//   NWN = 2: 4 (M) x 2 (N) warps of 32 x 32, producer warpgroup (setmaxnreg 104 / 24),
+//            2 CTAs / SM.
+template <int NWN>
+struct Warps {
+    static constexpr int WM = NWN == 4 ? 64 : 32, WN = 32;
+    static constexpr int NWM = BM / WM, NWW = 32 * NWN / WN;  // warps along M / along N
+    static constexpr int FM = WM / 8, FN = WN / 8;
+    static constexpr int NT = 32 * NWM * NWW;                 // MMA threads
+    static constexpr int PT = PRODUCER_THREADS;               // producer warpgroup
+    static_assert(NT == 256, "8 MMA warps");
+};
+
 template <int MODE, int NWN = 4>
 struct SmemPlan {
     static constexpr int BNT = 32 * NWN;
@@ -466,7 +482,7 @@ struct SmemPlan {
     static constexpr int PIPE_EL = NSTAGE * STAGE_EL + (MODE == MODE_FT_FUSED ? NSTAGE * 2 * BK : 0);
     // every mode stages the C tile ([BNT][LDT]) in the drained pipeline bytes; FT adds the
     // reduction arrays
-    static constexpr int EPI_FT = BNT * LDT + NWN * 3 * 128 + 2 * 3 * BNT + 2 * 256 + 128 + 136;
+    static constexpr int EPI_FT = BNT * LDT + Warps<NWN>::NWW * 3 * 128 + Warps<NWN>::NWM * 3 * BNT + 2 * 256 + 128 + 136;
     static constexpr int EPI = MODE != MODE_NOFT ? EPI_FT : BNT * LDT;
     static constexpr int EL = EPI > PIPE_EL ? EPI : PIPE_EL;
     static constexpr int BYTES = 8 * EL + 1024;  // + alignment slack
@@ -543,27 +559,29 @@ constexpr int LAUNCH_REGS = 168;
 constexpr int MMA_REGS = 224, PRODUCER_REGS = 56;  // 256x224 + 128x56 = 64512
 static_assert(NTHREADS * MMA_REGS + PRODUCER_THREADS * PRODUCER_REGS <= GEMM_THREADS * LAUNCH_REGS,
               "setmaxnreg budget exceeds the launch register allocation (would deadlock)");
-// Pair CTAs (2 per SM, 128 MMA + 128 producer threads): ptxas caps __launch_bounds__(256, 2) at
-// 128 registers, pool 256 x 128 = 32768 = 128 x 224 + 128 x 32.
-constexpr int PAIR_PRODUCER_REGS = 32;
-static_assert(128 * MMA_REGS + PRODUCER_THREADS * PAIR_PRODUCER_REGS <= 256 * 128, "pair setmaxnreg budget");
+// Pair CTAs (2 per SM, 256 MMA + 128 producer threads): __launch_bounds__(384, 2) starts every
+// thread at 80 registers (6 warps per SM sub-partition), pool 384 x 80 = 30720 >= 256 x 104 +
+// 128 x 24.
+constexpr int PAIR_MMA_REGS = 104, PAIR_PRODUCER_REGS = 24;
+static_assert(256 * PAIR_MMA_REGS + PRODUCER_THREADS * PAIR_PRODUCER_REGS <= 384 * 80, "pair setmaxnreg budget");
 
-// NWN = warps along N.  NWN = 4: one CTA per 128 x 128 tile (8 MMA warps, 1 CTA / SM).
-// NWN = 2 ("pair"): one CTA per 128 x 64 half of a 128 x 128 verification tile (4 MMA warps,
-// 2 CTAs / SM, so one CTA's epilogue overlaps the other's mainloop); for FT the two halves
+// NWN = 4: one CTA per 128 x 128 tile (8 MMA warps of 64 x 32, 1 CTA / SM).
+// NWN = 2 ("pair"): one CTA per 128 x 64 half of a 128 x 128 verification tile (8 MMA warps of
+// 32 x 32, 2 CTAs / SM, so one CTA's epilogue overlaps the other's mainloop); for FT the two halves
 // form a cluster of 2 and exchange their row partial sums and column-flag counts through
 // distributed shared memory, so verification, location and reports are those of the
 // 128 x 128 tile.
 template <bool KCA, bool KCB, bool TMA, int MODE, int NWN>
-__global__ void __launch_bounds__(64 * NWN + PRODUCER_THREADS, NWN == 2 ? 2 : 1)
+__global__ void __launch_bounds__(Warps<NWN>::NT + Warps<NWN>::PT, NWN == 2 ? 2 : 1)
     gemm_kernel(const __grid_constant__ GemmArgs g, const __grid_constant__ CUtensorMap tmA,
                 const __grid_constant__ CUtensorMap tmB) {
-    constexpr int NT = 64 * NWN;               // MMA threads
+    using WL = Warps<NWN>;
+    constexpr int NT = WL::NT, PT = WL::PT;    // MMA / producer threads
+    constexpr int WM = WL::WM, WN = WL::WN, FM = WL::FM, FN = WL::FN, NWM = WL::NWM, NWW = WL::NWW;
     constexpr int BNT = 32 * NWN;              // CTA tile columns
     constexpr bool FT = MODE != MODE_NOFT, FUSED = MODE == MODE_FT_FUSED;
     constexpr bool PAIR = NWN == 2 && FT;      // cluster pair sharing one verification tile
     static_assert(NWN == 4 || (NWN == 2 && !FUSED), "pair tiles: NOFT / FT_PRE only");
-    constexpr int PREG = NWN == 4 ? PRODUCER_REGS : PAIR_PRODUCER_REGS;
     extern __shared__ __align__(1024) double smem_raw[];
     __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES], norm_bar;
     // threshold norms of this tile (reading R4), reduced over the encode k-chunks by the
@@ -579,7 +597,7 @@ __global__ void __launch_bounds__(64 * NWN + PRODUCER_THREADS, NWN == 2 ? 2 : 1)
     // the loads below use 32-bit shared addressing)
     double *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) / 8u;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp & 1, wn = warp >> 1;
+    const int wm = warp % NWM, wn = warp / NWM;
     const long long ntm = (g.M + BM - 1) / BM, ntn = (g.N + BN - 1) / BN;  // 128 x 128 tiles
     long long tm, tn;
     tile_coords(NWN == 4 ? blockIdx.x : blockIdx.x >> 1, ntm, ntn, tm, tn);
@@ -599,17 +617,17 @@ __global__ void __launch_bounds__(64 * NWN + PRODUCER_THREADS, NWN == 2 ? 2 : 1)
         for (int s = 0; s < NS; s++) {
             // thread 0 of the producer arrives with expect_tx; cp.async fallback threads add
             // one arrival each when their copies land
-            mbar_init(&full_bar[s], 1 + (ALL_TMA ? 0 : PRODUCER_THREADS));
+            mbar_init(&full_bar[s], 1 + (ALL_TMA ? 0 : PT));
             mbar_init(&empty_bar[s], NT / 32);  // one arrival per MMA warp
         }
-        mbar_init(&norm_bar, PRODUCER_THREADS - 32);  // producer warps 1..3
+        mbar_init(&norm_bar, PT - 32);  // producer warps 1..3 (NWN = 4)
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
 
     if (warp >= NT / 32) {
         // ------------------------------------------------------------ producer warpgroup
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PREG));
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(NWN == 4 ? PRODUCER_REGS : PAIR_PRODUCER_REGS));
         const int pt = tid - NT;
         constexpr unsigned TX = (TMA_A ? TILE_EL * 8 : 0) + (TMA_B ? BNT * BK * 8 : 0) + (FUSED ? 2 * BK * 8 : 0);
         auto produce = [&](int kt) {
@@ -622,40 +640,35 @@ __global__ void __launch_bounds__(64 * NWN + PRODUCER_THREADS, NWN == 2 ? 2 : 1)
                     bulk_load(sV(st), g.VA + tm * g.Kp + k0, BK * 8, &full_bar[st]);
                 }
             }
-            produce_tile<KCA, TMA_A>(sA(st), &tmA, &full_bar[st], g.A, g.lda, m0, k0, g.M, g.K, pt);
-            produce_tile<KCB, TMA_B, BNT>(sB(st), &tmB, &full_bar[st], g.B, g.ldb, n0, k0, g.N, g.K, pt);
+            produce_tile<KCA, TMA_A, 128, PT>(sA(st), &tmA, &full_bar[st], g.A, g.lda, m0, k0, g.M, g.K, pt);
+            produce_tile<KCB, TMA_B, BNT, PT>(sB(st), &tmB, &full_bar[st], g.B, g.ldb, n0, k0, g.N, g.K, pt);
             if (!ALL_TMA) cp_async_mbar_arrive(&full_bar[st]);
         };
-        if (FT && pt >= 32) {
+        if (FT && NWN == 4 && pt >= 32) {
             // Threshold norms (reading R4) and, for FT_PRE, the checksum-GEMM slices of this tile,
             // by producer warps 1..3 while thread 0 streams the operand stages: quantity q < 128 is
             // row q, 128 <= q < 128 + BNT column q - 128 of this CTA, then the tile maxima of A / B.
-            // Sums over the encode k-chunks / the k-splits in fixed order, loads issued in batches.
-            // With FT_PRE the per-row / per-column values were summed once by side_finalize_kernel
-            // and are only copied here (FP64 arithmetic beside the DMMA stream costs several
-            // times its share); the fused mode sums the partials itself.
-            for (int q = pt - 32; q < 128 + BNT + 2; q += PRODUCER_THREADS - 32) {
-                // pair tiles (producer warps at 32 registers) copy finalized sums; 128 x 128 tiles
-                // sum the partials themselves and skip the finalize launch
-                constexpr bool fin = MODE == MODE_FT_PRE && NWN == 2;
+            // Sums over the encode k-chunks / the k-splits in fixed order, loads issued in batches
+            // (FP64 arithmetic off the MMA warps: beside the DMMA stream it costs several times its
+            // share).  Pair tiles copy the side_finalize_kernel sums instead
+            // (MMA threads, cp.async, below).
+            for (int q = pt - 32; q < 128 + BNT + 2; q += PT - 32) {
                 if (q < 128) {
                     const long long gi = m0 + q;
                     const bool ok = gi < g.M;
-                    nrm_row[q] = !ok ? 0.0 : fin ? g.fin_nrmA[gi] : sum_strided(g.lineA + gi, g.M, g.kch);
+                    nrm_row[q] = !ok ? 0.0 : sum_strided(g.lineA + gi, g.M, g.kch);
                     if (MODE == MODE_FT_PRE)
-                        pre_r[q] = !ok ? 0.0 : fin ? g.fin_R[tn * g.M + gi]
-                                                   : sum_strided(g.Rpre + tn * g.M + gi, g.stride_r, g.splits_r);
+                        pre_r[q] = !ok ? 0.0 : sum_strided(g.Rpre + tn * g.M + gi, g.stride_r, g.splits_r);
                 } else if (q < 128 + BNT) {
                     const long long gj = n0 + (q - 128);
                     const bool ok = gj < g.N;
-                    nrm_col[q - 128] = !ok ? 0.0 : fin ? g.fin_nrmB[gj] : sum_strided(g.lineB + gj, g.N, g.kch);
+                    nrm_col[q - 128] = !ok ? 0.0 : sum_strided(g.lineB + gj, g.N, g.kch);
                     if (MODE == MODE_FT_PRE)
-                        pre_s[q - 128] = !ok ? 0.0 : fin ? g.fin_S[tm * g.N + gj]
-                                                         : sum_strided(g.Spre + tm * g.N + gj, g.stride_s, g.splits_s);
+                        pre_s[q - 128] = !ok ? 0.0 : sum_strided(g.Spre + tm * g.N + gj, g.stride_s, g.splits_s);
                 } else if (q == 128 + BNT) {
-                    nrm_max[0] = fin ? g.fin_maxA[tm] : max_strided(g.tmaxA + tm, ntm, g.kch);
+                    nrm_max[0] = max_strided(g.tmaxA + tm, ntm, g.kch);
                 } else {
-                    nrm_max[1] = fin ? g.fin_maxB[tn] : max_strided(g.tmaxB + tn, ntn, g.kch);
+                    nrm_max[1] = max_strided(g.tmaxB + tn, ntn, g.kch);
                 }
             }
             mbar_arrive(&norm_bar);
@@ -683,8 +696,30 @@ __global__ void __launch_bounds__(64 * NWN + PRODUCER_THREADS, NWN == 2 ? 2 : 1)
         }
         return;
     }
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(MMA_REGS));
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(NWN == 4 ? MMA_REGS : PAIR_MMA_REGS));
     auto bar_mma = [&]() { asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory"); };
+    if (PAIR) {
+        // this half's finalized side data (side_finalize_kernel) -> smem by cp.async while the
+        // first operand stages are in flight; completed by the epilogue's cp.async wait
+        for (int q = tid; q < 128 + BNT + 2; q += NT) {
+            if (q < 128) {
+                const long long gi = m0 + q;
+                const bool ok = gi < g.M;
+                cp_async8(&nrm_row[q], ok ? g.fin_nrmA + gi : g.fin_nrmA, ok ? 8 : 0);
+                cp_async8(&pre_r[q], ok ? g.fin_R + tn * g.M + gi : g.fin_R, ok ? 8 : 0);
+            } else if (q < 128 + BNT) {
+                const long long gj = n0 + (q - 128);
+                const bool ok = gj < g.N;
+                cp_async8(&nrm_col[q - 128], ok ? g.fin_nrmB + gj : g.fin_nrmB, ok ? 8 : 0);
+                cp_async8(&pre_s[q - 128], ok ? g.fin_S + tm * g.N + gj : g.fin_S, ok ? 8 : 0);
+            } else if (q == 128 + BNT) {
+                cp_async8(&nrm_max[0], g.fin_maxA + tm, 8);
+            } else {
+                cp_async8(&nrm_max[1], g.fin_maxB + tn, 8);
+            }
+        }
+        cp_commit();
+    }
 
     double acc[FM][FN][2];
 #pragma unroll
@@ -720,7 +755,7 @@ __global__ void __launch_bounds__(64 * NWN + PRODUCER_THREADS, NWN == 2 ? 2 : 1)
             for (int a = 0; a < FM; a++)
 #pragma unroll
                 for (int b = 0; b < FN; b++) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
-            if (FUSED) {
+            if constexpr (FUSED) {
                 const double wk = w_s[k], vk = v_s[k];
                 // warp-uniform branches pick the fragment pair (no select temporaries)
                 if (wn == 0)      { rp[0] = fma(af[0], wk, rp[0]); rp[1] = fma(af[1], wk, rp[1]); }
@@ -824,16 +859,16 @@ __global__ void __launch_bounds__(64 * NWN + PRODUCER_THREADS, NWN == 2 ? 2 : 1)
 
     // -------------------------------------------------------------- FT epilogue
     // partial row sums [wn][q][128] and column sums [wm][q][BNT], q = 0: out, 1: C0, 2: |C0|
-    double *red_r = tileS + BNT * LDT;       // NWN x 3 x 128
-    double *red_c = red_r + NWN * 3 * 128;   // 2 x 3 x BNT
-    double *rsp = red_c + 2 * 3 * BNT, *ssp = rsp + 256, *dres = ssp + 256;
+    double *red_r = tileS + BNT * LDT;       // NWW x 3 x 128
+    double *red_c = red_r + NWW * 3 * 128;   // NWM x 3 x BNT
+    double *rsp = red_c + NWM * 3 * BNT, *ssp = rsp + 256, *dres = ssp + 256;
     int *flags = reinterpret_cast<int *>(dres + 128);  // [0] nrow, [1] ncol, [2..129] rows, [130..] cols
 
     // checksum reference: FUSED -- combine the 4 k-lanes of the mainloop partials (fixed order),
     // one writer per row / column; FT_PRE -- the checksum-GEMM slices staged by the producer
     // (read after the norm barrier below).  rsp[i] = r_i (row i of the C e column), ssp[j] = s_j
     // (column j of the e^T C row).
-    if (FUSED) {
+    if constexpr (FUSED) {
 #pragma unroll
         for (int t = 0; t < 2; t++) {
             rp[t] += __shfl_xor_sync(0xffffffffu, rp[t], 1);
@@ -875,24 +910,21 @@ __global__ void __launch_bounds__(64 * NWN + PRODUCER_THREADS, NWN == 2 ? 2 : 1)
     }
     // One pass over this thread's fragment elements: out = alpha acc + beta C0 into the smem
     // tile (0 outside M x N), with the row sums (over the thread's 8 columns of a fragment
-    // row, then the 4 lanes of the row) and column sums (over the thread's 8 rows, then the
+    // row, then the 4 lanes of the row) and column sums (over the thread's FM rows, then the
     // 8 lanes of the column) of out, C0 and |C0| -- the reference sums of the computed tile
     // (formed "at register level") and the beta C encoding (reading R3).
+    // Column fragments outer: the column partials of one fragment are reduced and stored
+    // before the next, so only the FM row partials stay live beside the accumulators.
     {
-        double cs[FN][2], cc[FN][2], ca[FN][2];
+        double rs[3][FM];
 #pragma unroll
-        for (int b = 0; b < FN; b++) cs[b][0] = cs[b][1] = cc[b][0] = cc[b][1] = ca[b][0] = ca[b][1] = 0.0;
-        auto row_red = [&](double v, int q, int row) {
-            v += __shfl_xor_sync(0xffffffffu, v, 1);
-            v += __shfl_xor_sync(0xffffffffu, v, 2);
-            if ((lane & 3) == 0) red_r[(wn * 3 + q) * 128 + row] = v;
-        };
+        for (int a = 0; a < FM; a++) rs[0][a] = rs[1][a] = rs[2][a] = 0.0;
 #pragma unroll
-        for (int a = 0; a < FM; a++) {
-            const int row = row_of(a);
-            double rs = 0.0, rc = 0.0, ra = 0.0;
+        for (int b = 0; b < FN; b++) {
+            double cs[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-            for (int b = 0; b < FN; b++)
+            for (int a = 0; a < FM; a++) {
+                const int row = row_of(a);
 #pragma unroll
                 for (int e = 0; e < 2; e++) {
                     const int col = col_of(b, e);
@@ -903,107 +935,143 @@ __global__ void __launch_bounds__(64 * NWN + PRODUCER_THREADS, NWN == 2 ? 2 : 1)
                     } else {
                         const double c0 = tileS[row + col * LDT];  // 0 outside M x N (zero-filled)
                         o = fma(g.alpha, acc[a][b][e], g.beta * c0);
-                        rc += c0; ra += fabs(c0);
-                        cc[b][e] += c0; ca[b][e] += fabs(c0);
+                        rs[1][a] += c0; rs[2][a] += fabs(c0);
+                        cs[1][e] += c0; cs[2][e] += fabs(c0);
                     }
                     o = ok ? o : 0.0;
                     tileS[row + col * LDT] = o;
-                    rs += o;
-                    cs[b][e] += o;
+                    rs[0][a] += o;
+                    cs[0][e] += o;
                 }
-            row_red(rs, 0, row);
-            if (!beta0) { row_red(rc, 1, row); row_red(ra, 2, row); }
+            }
+            // column sums over the 8 lanes of a fragment column (lane bits 2..4), transposing
+            // first step: lane keeps 3 of the 6 (q, e) values, v index = 2 q + e
+            {
+                const bool hi = lane & 4;
+                double x[3];
+#pragma unroll
+                for (int p = 0; p < 3; p++) {
+                    const double lo_v = cs[(p) >> 1][(p) & 1], hi_v = cs[(p + 3) >> 1][(p + 3) & 1];
+                    x[p] = (hi ? hi_v : lo_v) + __shfl_xor_sync(0xffffffffu, hi ? lo_v : hi_v, 4);
+                }
+#pragma unroll
+                for (int p = 0; p < 3; p++) {
+                    x[p] += __shfl_xor_sync(0xffffffffu, x[p], 8);
+                    x[p] += __shfl_xor_sync(0xffffffffu, x[p], 16);
+                }
+                if ((lane & 24) == 0) {
+#pragma unroll
+                    for (int p = 0; p < 3; p++) {
+                        const int t = p + (hi ? 3 : 0), q = t >> 1, e = t & 1;
+                        red_c[(wm * 3 + q) * BNT + col_of(b, e)] = x[p];
+                    }
+                }
+            }
         }
-        auto col_red = [&](double (&v)[FN][2], int q) {
+        // row sums over the 4 lanes of a fragment row (lane bits 0, 1), transposing: the 3 FM
+        // values (index q FM + a) halve twice; lane keeps indices 3FM/2 b0 + 3FM/4 b1 + p
+        {
+            constexpr int V = 3 * FM, H = V / 2, Q = V / 4;
+            const bool b0 = lane & 1, b1 = lane & 2;
+            double w[H], x[Q];
 #pragma unroll
-            for (int b = 0; b < FN; b++)
+            for (int p = 0; p < H; p++) {
+                const double lo_v = rs[p / FM][p % FM], hi_v = rs[(p + H) / FM][(p + H) % FM];
+                w[p] = (b0 ? hi_v : lo_v) + __shfl_xor_sync(0xffffffffu, b0 ? lo_v : hi_v, 1);
+            }
 #pragma unroll
-                for (int e = 0; e < 2; e++) {
-                    double x = v[b][e];
-                    x += __shfl_xor_sync(0xffffffffu, x, 4);
-                    x += __shfl_xor_sync(0xffffffffu, x, 8);
-                    x += __shfl_xor_sync(0xffffffffu, x, 16);
-                    if (lane < 4) red_c[(wm * 3 + q) * BNT + col_of(b, e)] = x;
-                }
-        };
-        col_red(cs, 0);
-        if (!beta0) { col_red(cc, 1); col_red(ca, 2); }
+            for (int p = 0; p < Q; p++)
+                x[p] = (b1 ? w[p + Q] : w[p]) + __shfl_xor_sync(0xffffffffu, b1 ? w[p] : w[p + Q], 2);
+#pragma unroll
+            for (int p = 0; p < Q; p++) {
+                const int t = p + (b0 ? H : 0) + (b1 ? Q : 0), q = t / FM, a = t % FM;
+                red_r[(wn * 3 + q) * 128 + row_of(a)] = x[p];
+            }
+        }
     }
+    if (PAIR) cp_wait<0>();  // this thread's side-data copies (beta = 0 has no C0 staging wait)
     bar_mma();
     // verification: flag rows / columns beyond the round-off threshold
     const double aa = fabs(g.alpha), ab = fabs(g.beta);
-    mbar_wait(&norm_bar, 0);  // producer-reduced norms are in nrm_row / nrm_col / nrm_max
+    if (!PAIR) mbar_wait(&norm_bar, 0);  // producer-reduced norms are in nrm_row / nrm_col / nrm_max
     // row sums of this CTA's columns (wn partials in fixed order); PAIR: exchanged with the
     // peer half through distributed shared memory and added in half order (h0 + h1), so both
     // CTAs hold the identical sums of the whole 128-wide tile
     auto rsum_local = [&](int q, int r) {
         double v = red_r[(0 * 3 + q) * 128 + r];
 #pragma unroll
-        for (int w = 1; w < NWN; w++) v += red_r[(w * 3 + q) * 128 + r];
+        for (int w = 1; w < NWW; w++) v += red_r[(w * 3 + q) * 128 + r];
         return v;
     };
-    if (PAIR) {
-        const unsigned peer = (unsigned)(half ^ 1);
-        for (int r = tid; r < BM; r += NT)
-#pragma unroll
-            for (int q = 0; q < 3; q++) {
-                const double v = rsum_local(q, r);
-                st_cluster_f64(&peer_rows[q * BM + r], peer, v);
-            }
-        cluster_sync();
-    }
     auto rsum = [&](int q, int r) {
         if (!PAIR) return rsum_local(q, r);
         const double mine = rsum_local(q, r), theirs = peer_rows[q * BM + r];
         return half == 0 ? mine + theirs : theirs + mine;
     };
-    for (int qq = tid; qq < BM + BNT; qq += NT) {
-        if (qq < BM) {
-            const int r = qq;
-            if (r < mvalid) {
-                const double sum = rsum(0, r);
-                const double rr2 = FUSED ? rsp[r] : pre_r[r];
-                const double c0s = beta0 ? 0.0 : rsum(1, r);
-                const double c0a = beta0 ? 0.0 : rsum(2, r);
-                const double ref = beta0 ? g.alpha * rr2 : fma(g.alpha, rr2, g.beta * c0s);
-                const double rowabs = nrm_row[r], bmax = nrm_max[1];
-                const double tau = 4.0 * U_ROUND * (double)(g.K + tvalid + 3) * (aa * rowabs * bmax + ab * c0a);
-                const double d = sum - ref;
-                dres[r] = d;
-                if (!(fabs(d) <= tau)) {
-                    const int p = atomicAdd(&flags[0], 1);
-                    flags[2 + p] = r;
-                }
+    auto verify_row = [&](int r) {
+        if (r >= mvalid) return;
+        const double sum = rsum(0, r);
+        const double rr2 = FUSED ? rsp[r] : pre_r[r];
+        const double c0s = beta0 ? 0.0 : rsum(1, r);
+        const double c0a = beta0 ? 0.0 : rsum(2, r);
+        const double ref = beta0 ? g.alpha * rr2 : fma(g.alpha, rr2, g.beta * c0s);
+        const double rowabs = nrm_row[r], bmax = nrm_max[1];
+        const double tau = 4.0 * U_ROUND * (double)(g.K + tvalid + 3) * (aa * rowabs * bmax + ab * c0a);
+        const double d = sum - ref;
+        dres[r] = d;
+        if (!(fabs(d) <= tau)) {
+            const int p = atomicAdd(&flags[0], 1);
+            flags[2 + p] = r;
+        }
+    };
+    auto verify_col = [&](int c) {  // all 128 rows of a column are in this CTA
+        if (c >= nvalid) return;
+        auto csum = [&](int q) {
+            double v = red_c[(0 * 3 + q) * BNT + c];
+#pragma unroll
+            for (int w = 1; w < NWM; w++) v += red_c[(w * 3 + q) * BNT + c];
+            return v;
+        };
+        const double sum = csum(0);
+        const double ss2 = FUSED ? ssp[c] : pre_s[c];
+        const double c0s = beta0 ? 0.0 : csum(1);
+        const double c0a = beta0 ? 0.0 : csum(2);
+        const double ref = beta0 ? g.alpha * ss2 : fma(g.alpha, ss2, g.beta * c0s);
+        const double colabs = nrm_col[c], amax = nrm_max[0];
+        const double tau = 4.0 * U_ROUND * (double)(g.K + mvalid + 3) * (aa * amax * colabs + ab * c0a);
+        const double d = sum - ref;
+        if (!(fabs(d) <= tau)) {
+            const int p = atomicAdd(&flags[1], 1);
+            flags[130 + p] = c;
+        }
+    };
+    if (PAIR) {
+        // one cluster barrier per tile: the columns are verified before the exchange, so the
+        // column-flag count travels with the row partial sums
+        const unsigned peer = (unsigned)(half ^ 1);
+        for (int qq = tid; qq < BM + BNT; qq += NT) {
+            if (qq < BM) {
+#pragma unroll
+                for (int q = 0; q < 3; q++) st_cluster_f64(&peer_rows[q * BM + qq], peer, rsum_local(q, qq));
+            } else {
+                verify_col(qq - BM);
             }
-        } else {
-            const int c = qq - BM;
-            if (c < nvalid) {
-                auto csum = [&](int q) { return red_c[(0 * 3 + q) * BNT + c] + red_c[(1 * 3 + q) * BNT + c]; };
-                const double sum = csum(0);
-                const double ss2 = FUSED ? ssp[c] : pre_s[c];
-                const double c0s = beta0 ? 0.0 : csum(1);
-                const double c0a = beta0 ? 0.0 : csum(2);
-                const double ref = beta0 ? g.alpha * ss2 : fma(g.alpha, ss2, g.beta * c0s);
-                const double colabs = nrm_col[c], amax = nrm_max[0];
-                const double tau = 4.0 * U_ROUND * (double)(g.K + mvalid + 3) * (aa * amax * colabs + ab * c0a);
-                const double d = sum - ref;
-                if (!(fabs(d) <= tau)) {
-                    const int p = atomicAdd(&flags[1], 1);
-                    flags[130 + p] = c;
-                }
-            }
+        }
+        bar_mma();
+        if (tid == 0) st_cluster_s32(&peer_nc, peer, flags[1]);
+        cluster_sync();
+        for (int r = tid; r < BM; r += NT) verify_row(r);
+    } else {
+        for (int qq = tid; qq < BM + BNT; qq += NT) {
+            if (qq < BM) verify_row(qq);
+            else verify_col(qq - BM);
         }
     }
     bar_mma();
     // nr: flagged rows of the verification tile (identical in both halves); nc: flagged columns
     // of this CTA; nct: flagged columns of the whole tile (PAIR: + the peer's count)
     const int nr = flags[0], nc = flags[1];
-    int nct = nc;
-    if (PAIR) {
-        if (tid == 0) st_cluster_s32(&peer_nc, (unsigned)(half ^ 1), nc);
-        cluster_sync();
-        nct = nc + peer_nc;
-    }
+    const int nct = PAIR ? nc + peer_nc : nc;
     if (nr != 0 || nct != 0) {
         // ---------------------------------------------------------- locate + correct (rare)
         if (tid == 0) {

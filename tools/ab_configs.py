@@ -24,7 +24,8 @@ for spec in libs:
         L.ftblas_set_tile_policy.argtypes = [ct.c_int]
         L.ftblas_set_tile_policy({"auto": 0, "full": 1, "pair": 2}[policy])
     Ls.append((os.path.basename(path) + (":" + policy if policy else ""), L))
-for w in syn.CONFIGS[:4]:
+SEL = os.environ.get("CONFIGS")
+for w in [c for c in syn.CONFIGS[:4] if not SEL or c.name.split("_")[0] in SEL.split(",")]:
     M, N, K = w.M, w.N, w.K
     lda = M if w.transA == "N" else K; ldb = K if w.transB == "N" else N
     A = torch.rand(M * K, dtype=torch.float64, device="cuda") * 2 - 1

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Microbenchmark: the consumer side of the DMMA mainloop alone (operand tiles resident in
 // smem, no global traffic, no pipeline waits), to separate the instruction-stream limit of
 // the fragment-load + DMMA.8x8x4 schedule from the memory pipeline.  Development evidence
@@ -325,6 +326,66 @@ int run_nw(const char *name, int sms, double *out, int blocks_per_sm, int stages
     return 0;
 }
 
+// CTA tile 128 x BNT with (128 / WM) x (BNT / WN) warps of WM x WN; MINB CTAs per SM.
+template <int WM, int WN, int BNT, int MINB>
+__global__ void __launch_bounds__((128 / WM) * (BNT / WN) * 32, MINB) mainloop_g(double *out, int ktiles) {
+    extern __shared__ double smem[];
+    constexpr int NWM = 128 / WM, FM = WM / 8, FN = WN / 8;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp % NWM, wn = warp / NWM;
+    constexpr int A_EL = BK * LD_MN, B_EL = BNT * LD_K, ST = A_EL + B_EL;
+    for (int i = tid; i < STAGES * ST; i += blockDim.x) smem[i] = 1.0 + 1e-3 * (i & 63);
+    __syncthreads();
+    double acc[FM][FN][2];
+#pragma unroll
+    for (int a = 0; a < FM; a++)
+#pragma unroll
+        for (int b = 0; b < FN; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int kt = 0; kt < ktiles; kt++) {
+        const double *as = smem + (kt % STAGES) * ST, *bs = as + A_EL;
+#pragma unroll
+        for (int kk = 0; kk < BK / 4; kk++) {
+            double af[FM], bf[FN];
+            const int k = kk * 4 + (lane & 3);
+#pragma unroll
+            for (int f = 0; f < FM; f++) af[f] = as[k * LD_MN + wm * WM + f * 8 + (lane >> 2)];
+#pragma unroll
+            for (int f = 0; f < FN; f++) bf[f] = bs[(wn * WN + f * 8 + (lane >> 2)) * LD_K + k];
+#pragma unroll
+            for (int a = 0; a < FM; a++)
+#pragma unroll
+                for (int b = 0; b < FN; b++) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        }
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a < FM; a++)
+#pragma unroll
+        for (int b = 0; b < FN; b++) s += acc[a][b][0] + acc[a][b][1];
+    out[blockIdx.x * blockDim.x + tid] = s;
+}
+
+template <int WM, int WN, int BNT, int MINB>
+int run_g(const char *name, int sms, double *out, int blocks_per_sm) {
+    auto k = mainloop_g<WM, WN, BNT, MINB>;
+    constexpr int NT = (128 / WM) * (BNT / WN) * 32;
+    const int bytes = STAGES * (BK * LD_MN + BNT * LD_K) * 8;
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    const int ktiles = 4096, blocks = sms * blocks_per_sm * 4;
+    k<<<blocks, NT, bytes>>>(out, 64);
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    k<<<blocks, NT, bytes>>>(out, ktiles);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    const double fl = 2.0 * 128 * BNT * BK * (double)ktiles * blocks;
+    printf("%-34s %8.3f ms  %6.2f TFLOP/s\n", name, ms, fl / ms / 1e9);
+    return 0;
+}
+
 int main() {
     cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
     printf("device %s sms=%d\n", p.name, p.multiProcessorCount);
@@ -339,6 +400,15 @@ int main() {
     run_nw<4, 1>("8 warps 128x128, 1 CTA/SM", sms, out, 1, 1);
     run_nw<2, 1>("4 warps 128x64, 1 CTA/SM", sms, out, 1, 1);
     run_nw<2, 2>("4 warps 128x64, 2 CTA/SM", sms, out, 2, 1);
+    if (getenv("PAIR_ONLY")) {
+        run_g<64, 32, 64, 1>("g 4 warps 64x32 128x64 1 CTA/SM", sms, out, 1);
+        run_g<64, 32, 64, 2>("g 4 warps 64x32 128x64 2 CTA/SM", sms, out, 2);
+        run_g<32, 32, 64, 1>("g 8 warps 32x32 128x64 1 CTA/SM", sms, out, 1);
+        run_g<32, 32, 64, 2>("g 8 warps 32x32 128x64 2 CTA/SM", sms, out, 2);
+        run_g<64, 16, 64, 1>("g 8 warps 64x16 128x64 1 CTA/SM", sms, out, 1);
+        run_g<32, 64, 64, 1>("g 4 warps 32x64 128x64 1 CTA/SM", sms, out, 1);
+        return 0;
+    }
     run_cw<4, 0>("8 MMA + 4 cksum warps LDS+DFMA", sms, out);
     run_cw<4, 1>("8 MMA + 4 cksum warps LDS only", sms, out);
     run_cw<4, 2>("8 MMA + 4 cksum warps DFMA only", sms, out);
