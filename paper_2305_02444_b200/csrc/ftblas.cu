@@ -332,7 +332,9 @@ cudaError_t launch_cksum_t(const CkArgs &a, const CUtensorMap &mx, const CUtenso
 // total, at least one BK slice per split.
 void cksum_split(long long tiles, long long K, long long &splits, long long &kper) {
     const long long kt = std::max<long long>(1, (K + BK - 1) / BK);
-    splits = std::max<long long>(1, std::min<long long>(kt, (4 * 148 + tiles - 1) / tiles));
+    // about 4 waves of CTAs, but every split at least 16 k-tiles deep: for small K the partial
+    // outputs (splits x P x Q doubles, written and re-read) would cost more than the DMMAs
+    splits = std::max<long long>(1, std::min<long long>({kt / 16, (4 * 148 + tiles - 1) / tiles}));
     kper = (kt + splits - 1) / splits * BK;
     splits = (K + kper - 1) / kper;
 }
@@ -451,7 +453,10 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
         double *Rpre = w + oR, *Spre = w + oS;
         double *fin = w + oF;
         g.fin_nrmA = fin; g.fin_nrmB = fin + M; g.fin_maxA = fin + M + N; g.fin_maxB = fin + M + N + ntm;
-        g.fin_R = fin + M + N + ntm + ntn; g.fin_S = g.fin_R + (size_t)ntn * M;
+        // one k-split each: the checksum GEMM outputs are final, the pair tiles read them in place
+        const bool rs_final = spR == 1 && spS == 1;
+        g.fin_R = rs_final ? Rpre : fin + M + N + ntm + ntn;
+        g.fin_S = rs_final ? Spre : g.fin_R + (size_t)ntn * M;
         g.Rpre = pre ? Rpre : nullptr;
         g.Spre = pre ? Spre : nullptr;
         g.splits_r = (int)spR; g.splits_s = (int)spS;
@@ -503,12 +508,13 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
             // per-row / per-column side data of the verification: partials summed once (the
             // pair-tile producers copy them; 128 x 128 tiles sum the partials in the producer)
             FinArgs fa{};
-            fa.lineA = lineA; fa.lineB = lineB; fa.tmaxA = tmaxA; fa.tmaxB = tmaxB; fa.Rp = Rpre; fa.Sp = Spre;
+            fa.lineA = lineA; fa.lineB = lineB; fa.tmaxA = tmaxA; fa.tmaxB = tmaxB;
+            fa.Rp = rs_final ? nullptr : Rpre; fa.Sp = rs_final ? nullptr : Spre;  // nullptr: nothing to sum
             fa.M = M; fa.N = N; fa.ntm = ntm; fa.ntn = ntn; fa.stride_r = g.stride_r; fa.stride_s = g.stride_s;
             fa.kch = kch; fa.splits_r = (int)spR; fa.splits_s = (int)spS;
             fa.nrmA = fin; fa.nrmB = fin + M; fa.maxA = fin + M + N; fa.maxB = fin + M + N + ntm;
             fa.R = fin + M + N + ntm + ntn; fa.S = fa.R + (size_t)ntn * M;
-            const long long total = (long long)nF;
+            const long long total = (long long)(M + N + ntm + ntn) + (rs_final ? 0 : (long long)ntn * M + (long long)ntm * N);
             const unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 8 * 148);
             side_finalize_kernel<<<blocks, 256, 0, c.stream>>>(fa);
             c.launches++;

@@ -1136,7 +1136,8 @@ struct FinArgs {
     double *nrmA, *nrmB, *maxA, *maxB, *R, *S;
 };
 __global__ void __launch_bounds__(256) side_finalize_kernel(FinArgs f) {
-    const long long nA = f.M, nB = f.N, nmA = f.ntm, nmB = f.ntn, nR = f.ntn * f.M, nS = f.ntm * f.N;
+    const long long nA = f.M, nB = f.N, nmA = f.ntm, nmB = f.ntn;
+    const long long nR = f.Rp ? f.ntn * f.M : 0, nS = f.Sp ? f.ntm * f.N : 0;  // nullptr: already final
     const long long total = nA + nB + nmA + nmB + nR + nS;
     for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (long long)gridDim.x * blockDim.x) {
         long long y = x;
