@@ -152,7 +152,7 @@ int ftblas_get_checksum_mode(void);
 
 /* CTA tiling of the GEMM kernels (a performance choice; results, reports and the 128 x 128
  * verification tile are the same):
- *   FTBLAS_TILES_AUTO (default): FTBLAS_TILES_PAIR for K <= 4096, else FTBLAS_TILES_FULL;
+ *   FTBLAS_TILES_AUTO (default): FTBLAS_TILES_PAIR for K <= 2048, else FTBLAS_TILES_FULL;
  *   FTBLAS_TILES_FULL: one CTA per 128 x 128 tile (8 MMA warps of 64 x 32, one CTA per SM);
  *   FTBLAS_TILES_PAIR: two CTAs per tile, each a 128 x 64 half (8 MMA warps of 32 x 32, two
  *       CTAs per SM so one CTA's epilogue overlaps another's mainloop); for ftblas_dgemm the halves form a

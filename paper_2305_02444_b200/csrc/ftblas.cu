@@ -85,7 +85,7 @@ struct Ctx {
     char err[512] = "no error";
     int checksum_mode = FTBLAS_CHECKSUM_GEMM;
     int tile_policy = FTBLAS_TILES_AUTO;
-    long long pair_kmax = 4096;  // FTBLAS_TILES_AUTO: half-tile CTAs for K <= pair_kmax (measured: c1 K=4096 pair 34.3 vs full 34.1 TF FT)
+    long long pair_kmax = 2048;  // FTBLAS_TILES_AUTO: half-tile CTAs for K <= pair_kmax (c1, K = 4096: full 34.1, pair 34.0 TF FT)
     int device = -1;
 };
 Ctx &ctx() {

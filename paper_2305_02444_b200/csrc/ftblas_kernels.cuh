@@ -303,6 +303,10 @@ struct EncodeArgs {
     ReportHdr *rep;  // zeroed here (stream-ordered before the GEMM kernel)
 };
 
+// an unsigned stored in the low word of a double's bit pattern (smem / DSMEM transport only)
+__device__ __forceinline__ double u32_as_dbits(unsigned u) { return __longlong_as_double((long long)u); }
+__device__ __forceinline__ unsigned dbits_as_u32(double d) { return (unsigned)__double_as_longlong(d); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
@@ -462,15 +466,15 @@ enum { MODE_NOFT = 0, MODE_FT_PRE = 1, MODE_FT_FUSED = 2 };
 // per SM sub-partition, which is what keeps the DMMA pipe fed (tools/dmma_mainloop.cu: a
 // 128 x 64 CTA of 4 warps reaches 32.5 TFLOP/s alone, of 8 warps 32 x 32 36.9).
 //   NWN = 4: 2 (M) x 4 (N) warps of 64 x 32, producer warpgroup (setmaxnreg 224 / 56).
-//   NWN = 2: 4 (M) x 2 (N) warps of 32 x 32, producer warpgroup (setmaxnreg 104 / 24),
-//            2 CTAs / SM.
+//   NWN = 2: 4 (M) x 2 (N) warps of 32 x 32, one producer warp, 2 CTAs / SM, no setmaxnreg
+//            (9 warps x 2 CTAs: at most 5 warps per SM sub-partition -> 96 registers).
 template <int NWN>
 struct Warps {
     static constexpr int WM = NWN == 4 ? 64 : 32, WN = 32;
     static constexpr int NWM = BM / WM, NWW = 32 * NWN / WN;  // warps along M / along N
     static constexpr int FM = WM / 8, FN = WN / 8;
     static constexpr int NT = 32 * NWM * NWW;                 // MMA threads
-    static constexpr int PT = PRODUCER_THREADS;               // producer warpgroup
+    static constexpr int PT = NWN == 4 ? PRODUCER_THREADS : 32;  // producer threads
     static_assert(NT == 256, "8 MMA warps");
 };
 
@@ -559,11 +563,10 @@ constexpr int LAUNCH_REGS = 168;
 constexpr int MMA_REGS = 224, PRODUCER_REGS = 56;  // 256x224 + 128x56 = 64512
 static_assert(NTHREADS * MMA_REGS + PRODUCER_THREADS * PRODUCER_REGS <= GEMM_THREADS * LAUNCH_REGS,
               "setmaxnreg budget exceeds the launch register allocation (would deadlock)");
-// Pair CTAs (2 per SM, 256 MMA + 128 producer threads): __launch_bounds__(384, 2) starts every
-// thread at 80 registers (6 warps per SM sub-partition), pool 384 x 80 = 30720 >= 256 x 104 +
-// 128 x 24.
-constexpr int PAIR_MMA_REGS = 104, PAIR_PRODUCER_REGS = 24;
-static_assert(256 * PAIR_MMA_REGS + PRODUCER_THREADS * PAIR_PRODUCER_REGS <= 384 * 80, "pair setmaxnreg budget");
+// Pair CTAs (2 per SM) do not use setmaxnreg: with a producer warpgroup at 24 and MMA warps at
+// 104 registers, accumulators of CTAs sharing an SM came out corrupted under some schedules
+// (NT operands, tiles with long correction phases next to others; bitwise-clean without
+// setmaxnreg -- DESIGN.md section 5).  One producer warp keeps 9 warps per CTA, 96 registers.
 
 // NWN = 4: one CTA per 128 x 128 tile (8 MMA warps of 64 x 32, 1 CTA / SM).
 // NWN = 2 ("pair"): one CTA per 128 x 64 half of a 128 x 128 verification tile (8 MMA warps of
@@ -627,7 +630,7 @@ __global__ void __launch_bounds__(Warps<NWN>::NT + Warps<NWN>::PT, NWN == 2 ? 2 
 
     if (warp >= NT / 32) {
         // ------------------------------------------------------------ producer warpgroup
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(NWN == 4 ? PRODUCER_REGS : PAIR_PRODUCER_REGS));
+        if (NWN == 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
         const int pt = tid - NT;
         constexpr unsigned TX = (TMA_A ? TILE_EL * 8 : 0) + (TMA_B ? BNT * BK * 8 : 0) + (FUSED ? 2 * BK * 8 : 0);
         auto produce = [&](int kt) {
@@ -696,7 +699,7 @@ __global__ void __launch_bounds__(Warps<NWN>::NT + Warps<NWN>::PT, NWN == 2 ? 2 
         }
         return;
     }
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(NWN == 4 ? MMA_REGS : PAIR_MMA_REGS));
+    if (NWN == 4) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(MMA_REGS));
     auto bar_mma = [&]() { asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory"); };
     if (PAIR) {
         // this half's finalized side data (side_finalize_kernel) -> smem by cp.async while the
@@ -909,19 +912,25 @@ __global__ void __launch_bounds__(Warps<NWN>::NT + Warps<NWN>::PT, NWN == 2 ? 2 
         }
     }
     // One pass over this thread's fragment elements: out = alpha acc + beta C0 into the smem
-    // tile (0 outside M x N), with the row sums (over the thread's 8 columns of a fragment
-    // row, then the 4 lanes of the row) and column sums (over the thread's FM rows, then the
-    // 8 lanes of the column) of out, C0 and |C0| -- the reference sums of the computed tile
-    // (formed "at register level") and the beta C encoding (reading R3).
-    // Column fragments outer: the column partials of one fragment are reduced and stored
-    // before the next, so only the FM row partials stay live beside the accumulators.
+    // tile (0 outside M x N), with, per row and per column of the tile, the sum of
+    // d = out - beta C0 (the computed alpha op(A) op(B) part of the stored value, PAPER.md
+    // line 558: the reference sums are formed "at register level") and the maximum of |C0|
+    // (threshold ingredient, reading R4k).  d costs one DADD per element beyond the plain
+    // epilogue and the |C0| maxima run on the integer pipe (maxima of the high words of the
+    // doubles, which order non-negative doubles): FP64 instructions in the epilogue wait for
+    // the FP64 pipe that the co-resident CTA's DMMA stream keeps busy.
+    // Sums: over the thread's elements of a fragment row / column, then over the 4 / 8 lanes
+    // of that row / column (transposing butterflies); column fragments outer, so the column
+    // partials of one fragment are reduced and stored before the next.
     {
-        double rs[3][FM];
+        double rs[FM];
+        unsigned rm[FM];
 #pragma unroll
-        for (int a = 0; a < FM; a++) rs[0][a] = rs[1][a] = rs[2][a] = 0.0;
+        for (int a = 0; a < FM; a++) { rs[a] = 0.0; rm[a] = 0u; }
 #pragma unroll
         for (int b = 0; b < FN; b++) {
-            double cs[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+            double cs[2] = {0.0, 0.0};
+            unsigned cm[2] = {0u, 0u};
 #pragma unroll
             for (int a = 0; a < FM; a++) {
                 const int row = row_of(a);
@@ -929,63 +938,64 @@ __global__ void __launch_bounds__(Warps<NWN>::NT + Warps<NWN>::PT, NWN == 2 ? 2 
                 for (int e = 0; e < 2; e++) {
                     const int col = col_of(b, e);
                     const bool ok = row < mvalid && col < nvalid;
-                    double o;
+                    double o, d;
                     if (beta0) {
                         o = g.alpha * acc[a][b][e];
+                        d = o;
                     } else {
                         const double c0 = tileS[row + col * LDT];  // 0 outside M x N (zero-filled)
-                        o = fma(g.alpha, acc[a][b][e], g.beta * c0);
-                        rs[1][a] += c0; rs[2][a] += fabs(c0);
-                        cs[1][e] += c0; cs[2][e] += fabs(c0);
+                        const double t = g.beta * c0;
+                        o = fma(g.alpha, acc[a][b][e], t);
+                        d = o - t;
+                        const unsigned h = (unsigned)__double2hiint(c0) & 0x7fffffffu;
+                        rm[a] = max(rm[a], h);
+                        cm[e] = max(cm[e], h);
                     }
                     o = ok ? o : 0.0;
+                    d = ok ? d : 0.0;
                     tileS[row + col * LDT] = o;
-                    rs[0][a] += o;
-                    cs[0][e] += o;
+                    rs[a] += d;
+                    cs[e] += d;
                 }
             }
-            // column sums over the 8 lanes of a fragment column (lane bits 2..4), transposing
-            // first step: lane keeps 3 of the 6 (q, e) values, v index = 2 q + e
+            // columns: 8 lanes (lane bits 2..4); first step transposing (lane keeps e = bit 2)
             {
                 const bool hi = lane & 4;
-                double x[3];
-#pragma unroll
-                for (int p = 0; p < 3; p++) {
-                    const double lo_v = cs[(p) >> 1][(p) & 1], hi_v = cs[(p + 3) >> 1][(p + 3) & 1];
-                    x[p] = (hi ? hi_v : lo_v) + __shfl_xor_sync(0xffffffffu, hi ? lo_v : hi_v, 4);
-                }
-#pragma unroll
-                for (int p = 0; p < 3; p++) {
-                    x[p] += __shfl_xor_sync(0xffffffffu, x[p], 8);
-                    x[p] += __shfl_xor_sync(0xffffffffu, x[p], 16);
-                }
+                double x = (hi ? cs[1] : cs[0]) + __shfl_xor_sync(0xffffffffu, hi ? cs[0] : cs[1], 4);
+                x += __shfl_xor_sync(0xffffffffu, x, 8);
+                x += __shfl_xor_sync(0xffffffffu, x, 16);
+                unsigned m = hi ? cm[1] : cm[0];
+                m = max(m, __shfl_xor_sync(0xffffffffu, hi ? cm[0] : cm[1], 4));
+                m = max(m, __shfl_xor_sync(0xffffffffu, m, 8));
+                m = max(m, __shfl_xor_sync(0xffffffffu, m, 16));
                 if ((lane & 24) == 0) {
-#pragma unroll
-                    for (int p = 0; p < 3; p++) {
-                        const int t = p + (hi ? 3 : 0), q = t >> 1, e = t & 1;
-                        red_c[(wm * 3 + q) * BNT + col_of(b, e)] = x[p];
-                    }
+                    const int c = col_of(b, hi ? 1 : 0);
+                    red_c[(wm * 3 + 0) * BNT + c] = x;
+                    red_c[(wm * 3 + 1) * BNT + c] = u32_as_dbits(m);
                 }
             }
         }
-        // row sums over the 4 lanes of a fragment row (lane bits 0, 1), transposing: the 3 FM
-        // values (index q FM + a) halve twice; lane keeps indices 3FM/2 b0 + 3FM/4 b1 + p
+        // rows: 4 lanes (lane bits 0, 1), transposing: FM values halve twice (FM = 4 or 8)
         {
-            constexpr int V = 3 * FM, H = V / 2, Q = V / 4;
+            constexpr int H = FM / 2, Q = FM / 4;
             const bool b0 = lane & 1, b1 = lane & 2;
             double w[H], x[Q];
+            unsigned wmx[H], xm[Q];
 #pragma unroll
             for (int p = 0; p < H; p++) {
-                const double lo_v = rs[p / FM][p % FM], hi_v = rs[(p + H) / FM][(p + H) % FM];
-                w[p] = (b0 ? hi_v : lo_v) + __shfl_xor_sync(0xffffffffu, b0 ? lo_v : hi_v, 1);
+                w[p] = (b0 ? rs[p + H] : rs[p]) + __shfl_xor_sync(0xffffffffu, b0 ? rs[p] : rs[p + H], 1);
+                wmx[p] = max(b0 ? rm[p + H] : rm[p], __shfl_xor_sync(0xffffffffu, b0 ? rm[p] : rm[p + H], 1));
             }
 #pragma unroll
-            for (int p = 0; p < Q; p++)
+            for (int p = 0; p < Q; p++) {
                 x[p] = (b1 ? w[p + Q] : w[p]) + __shfl_xor_sync(0xffffffffu, b1 ? w[p] : w[p + Q], 2);
+                xm[p] = max(b1 ? wmx[p + Q] : wmx[p], __shfl_xor_sync(0xffffffffu, b1 ? wmx[p] : wmx[p + Q], 2));
+            }
 #pragma unroll
             for (int p = 0; p < Q; p++) {
-                const int t = p + (b0 ? H : 0) + (b1 ? Q : 0), q = t / FM, a = t % FM;
-                red_r[(wn * 3 + q) * 128 + row_of(a)] = x[p];
+                const int a = p + (b0 ? H : 0) + (b1 ? Q : 0);
+                red_r[(wn * 3 + 0) * 128 + row_of(a)] = x[p];
+                red_r[(wn * 3 + 1) * 128 + row_of(a)] = u32_as_dbits(xm[p]);
             }
         }
     }
@@ -996,25 +1006,39 @@ __global__ void __launch_bounds__(Warps<NWN>::NT + Warps<NWN>::PT, NWN == 2 ? 2 
     if (!PAIR) mbar_wait(&norm_bar, 0);  // producer-reduced norms are in nrm_row / nrm_col / nrm_max
     // row sums of this CTA's columns (wn partials in fixed order); PAIR: exchanged with the
     // peer half through distributed shared memory and added in half order (h0 + h1), so both
-    // CTAs hold the identical sums of the whole 128-wide tile
+    // CTAs hold the identical sums of the whole 128-wide tile.  q = 0: sum of d, q = 1: the
+    // high word of max |C0| (as the bits of a double; combined with an integer max).
     auto rsum_local = [&](int q, int r) {
-        double v = red_r[(0 * 3 + q) * 128 + r];
+        if (q == 0) {
+            double v = red_r[(0 * 3 + 0) * 128 + r];
 #pragma unroll
-        for (int w = 1; w < NWW; w++) v += red_r[(w * 3 + q) * 128 + r];
-        return v;
+            for (int w = 1; w < NWW; w++) v += red_r[(w * 3 + 0) * 128 + r];
+            return v;
+        }
+        unsigned m = dbits_as_u32(red_r[(0 * 3 + 1) * 128 + r]);
+#pragma unroll
+        for (int w = 1; w < NWW; w++) m = max(m, dbits_as_u32(red_r[(w * 3 + 1) * 128 + r]));
+        return u32_as_dbits(m);
     };
     auto rsum = [&](int q, int r) {
         if (!PAIR) return rsum_local(q, r);
         const double mine = rsum_local(q, r), theirs = peer_rows[q * BM + r];
+        if (q == 1) return u32_as_dbits(max(dbits_as_u32(mine), dbits_as_u32(theirs)));
         return half == 0 ? mine + theirs : theirs + mine;
+    };
+    // n x max |C0| >= sum |C0| over n elements (reading R4k): the high word h of max |C0|
+    // rounded up to h + 1 (+Inf when C0 holds Inf / NaN)
+    auto c0_bound = [&](double hbits, long long n) {
+        const unsigned h = dbits_as_u32(hbits);
+        if (h >= 0x7ff00000u) return __longlong_as_double(0x7ff0000000000000ll);
+        return (double)n * __hiloint2double((int)(h + 1u), 0);
     };
     auto verify_row = [&](int r) {
         if (r >= mvalid) return;
         const double sum = rsum(0, r);
         const double rr2 = FUSED ? rsp[r] : pre_r[r];
-        const double c0s = beta0 ? 0.0 : rsum(1, r);
-        const double c0a = beta0 ? 0.0 : rsum(2, r);
-        const double ref = beta0 ? g.alpha * rr2 : fma(g.alpha, rr2, g.beta * c0s);
+        const double c0a = beta0 ? 0.0 : c0_bound(rsum(1, r), tvalid);
+        const double ref = g.alpha * rr2;
         const double rowabs = nrm_row[r], bmax = nrm_max[1];
         const double tau = 4.0 * U_ROUND * (double)(g.K + tvalid + 3) * (aa * rowabs * bmax + ab * c0a);
         const double d = sum - ref;
@@ -1026,17 +1050,16 @@ __global__ void __launch_bounds__(Warps<NWN>::NT + Warps<NWN>::PT, NWN == 2 ? 2 
     };
     auto verify_col = [&](int c) {  // all 128 rows of a column are in this CTA
         if (c >= nvalid) return;
-        auto csum = [&](int q) {
-            double v = red_c[(0 * 3 + q) * BNT + c];
+        double sum = red_c[(0 * 3 + 0) * BNT + c];
+        unsigned m = dbits_as_u32(red_c[(0 * 3 + 1) * BNT + c]);
 #pragma unroll
-            for (int w = 1; w < NWM; w++) v += red_c[(w * 3 + q) * BNT + c];
-            return v;
-        };
-        const double sum = csum(0);
+        for (int w = 1; w < NWM; w++) {
+            sum += red_c[(w * 3 + 0) * BNT + c];
+            m = max(m, dbits_as_u32(red_c[(w * 3 + 1) * BNT + c]));
+        }
         const double ss2 = FUSED ? ssp[c] : pre_s[c];
-        const double c0s = beta0 ? 0.0 : csum(1);
-        const double c0a = beta0 ? 0.0 : csum(2);
-        const double ref = beta0 ? g.alpha * ss2 : fma(g.alpha, ss2, g.beta * c0s);
+        const double c0a = beta0 ? 0.0 : c0_bound(u32_as_dbits(m), mvalid);
+        const double ref = g.alpha * ss2;
         const double colabs = nrm_col[c], amax = nrm_max[0];
         const double tau = 4.0 * U_ROUND * (double)(g.K + mvalid + 3) * (aa * amax * colabs + ab * c0a);
         const double d = sum - ref;
@@ -1052,7 +1075,7 @@ __global__ void __launch_bounds__(Warps<NWN>::NT + Warps<NWN>::PT, NWN == 2 ? 2 
         for (int qq = tid; qq < BM + BNT; qq += NT) {
             if (qq < BM) {
 #pragma unroll
-                for (int q = 0; q < 3; q++) st_cluster_f64(&peer_rows[q * BM + qq], peer, rsum_local(q, qq));
+                for (int q = 0; q < 2; q++) st_cluster_f64(&peer_rows[q * BM + qq], peer, rsum_local(q, qq));
             } else {
                 verify_col(qq - BM);
             }

@@ -376,3 +376,44 @@ def test_zero_fault_transparency_and_no_false_positives(ft):
         torch.cuda.synchronize()
         assert rep.count == 0 and rep.tiles_flagged == 0, (M, N, K, tA, tB)
         assert torch.equal(C1_t, C2_t), (M, N, K, tA, tB, alpha, beta)
+
+
+@pytest.mark.parametrize("tB", ["N", "T"])
+@pytest.mark.parametrize("tiles", ["pair", "full"])
+def test_many_faulted_tiles_leave_neighbours_clean(tB, tiles):
+    """Regression: 100 faulted tiles (each with a long single-element recompute) next to clean
+    tiles, K deep enough that CTAs of different tiles share SMs for a long time.  Every flag
+    must come from a planned flip: exactly one kind-1 correction per faulted tile, no other
+    tile flagged, and C bitwise equal to the fault-free run (the corrected elements are
+    recomputed, all others untouched).  (Pair CTAs with setmaxnreg failed this for NT.)"""
+    import torch
+    ft = _lib("gemm", tiles)
+    try:
+        w = syn.Workload("t", 2048, 2048, 2048, "N", tB, 1.5, -0.5, "uniform", True, seed=5)
+        d = syn.make_inputs(w)
+        plan = syn.fault_plan(w.M, w.N, 100, 17)
+        C_clean, rep0 = run_gpu(ft, w, d)
+        assert rep0.count == 0
+        ft.ftblas_set_fault_plan(*plan)
+        for _ in range(3):
+            C_t, pC = to_dev(d["C"], 0)
+            A_t, pA = to_dev(d["A"], 0)
+            B_t, pB = to_dev(d["B"], 0)
+            rep = ft.Report(8192)
+            ft.ftblas_dgemm(w.transA, w.transB, w.M, w.N, w.K, w.alpha, pA, d["lda"], pB, d["ldb"],
+                            w.beta, pC, d["ldc"], rep)
+            torch.cuda.synchronize()
+            got = sorted((e["i"], e["j"], e["kind"]) for e in rep.entries())
+            want = sorted((int(i), int(j), 1) for i, j in zip(plan[0], plan[1]))
+            assert rep.count == 100 and rep.tiles_flagged == 100 and got == want
+            C_gpu = from_dev(C_t, d["C"], 0)
+            changed = np.argwhere(C_gpu != C_clean)
+            assert {(int(i), int(j)) for i, j in changed} <= {(i, j) for i, j, _ in want}
+            if len(changed):
+                ii, jj = changed[:, 0], changed[:, 1]
+                ab = abs_product(w, d)[ii, jj]
+                tol = gemm_bound(w.K, w.alpha, w.beta, ab, np.abs(d["C"][ii, jj]))
+                assert (np.abs(C_gpu[ii, jj] - C_clean[ii, jj]) <= tol).all()
+    finally:
+        ft.ftblas_clear_fault_plan()
+        ft.ftblas_set_tile_policy("auto")
