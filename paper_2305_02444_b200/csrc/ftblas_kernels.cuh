@@ -563,10 +563,11 @@ constexpr int LAUNCH_REGS = 168;
 constexpr int MMA_REGS = 224, PRODUCER_REGS = 56;  // 256x224 + 128x56 = 64512
 static_assert(NTHREADS * MMA_REGS + PRODUCER_THREADS * PRODUCER_REGS <= GEMM_THREADS * LAUNCH_REGS,
               "setmaxnreg budget exceeds the launch register allocation (would deadlock)");
-// Pair CTAs (2 per SM) do not use setmaxnreg: with a producer warpgroup at 24 and MMA warps at
-// 104 registers, accumulators of CTAs sharing an SM came out corrupted under some schedules
-// (NT operands, tiles with long correction phases next to others; bitwise-clean without
-// setmaxnreg -- DESIGN.md section 5).  One producer warp keeps 9 warps per CTA, 96 registers.
+// Pair CTAs (2 per SM) have one producer warp and no setmaxnreg: with a producer warpgroup
+// (with or without setmaxnreg) accumulators of CTAs sharing an SM came out corrupted under
+// some schedules (NT operands, tiles with long correction phases next to clean ones); the
+// one-warp variant is clean in every stress run (regression test
+// test_many_faulted_tiles_leave_neighbours_clean).  9 warps per CTA -> 96 registers.
 
 // NWN = 4: one CTA per 128 x 128 tile (8 MMA warps of 64 x 32, 1 CTA / SM).
 // NWN = 2 ("pair"): one CTA per 128 x 64 half of a 128 x 128 verification tile (8 MMA warps of
