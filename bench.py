@@ -36,6 +36,15 @@ DEFAULT_WORKLOAD = "c3_16384_sharded"
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 
 
+def base_config(w) -> dict:
+    """The workload keys both arms (ours and --impl reference) report."""
+    return {"workload": w.name, "M": w.M, "N": w.N, "K": w.K, "transA": w.transA,
+            "transB": w.transB, "alpha": w.alpha, "beta": w.beta,
+            "dist": {"uniform": "U[-1,1]", "normal": "N(0,1)"}[w.dist], "seed": w.seed,
+            "injected_flips": w.n_flips, "flip_bits": [syn.BIT_LO, syn.BIT_HI],
+            "verification_tile": [syn.TILE_M, syn.TILE_N]}
+
+
 def ratio_rule(achieved: float) -> dict:
     """The contraction peak by the task's ratio rule: measured bf16 (MEASURED_PEAKS.json) x the
     nominal FP64 / bf16 ratio of B200 (45 / 2250 TFLOP/s).  Reported beside the DMMA-measured
@@ -168,9 +177,8 @@ def run_reference(args, w):
            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "ms_per_step": 1e3 * step_s,
-           "config": {"workload": w.name, "M": w.M, "N": w.N, "K": w.K, "transA": w.transA,
-                      "transB": w.transB, "alpha": w.alpha, "beta": w.beta, "dist": w.dist,
-                      "seed": w.seed, "injected_flips": w.n_flips},
+           "config": dict(base_config(w), parallelism="CPU oracle, 1 thread, bounded tile sample per step",
+                          l2="n/a (host)"),
            "cpu_baseline": cb,
            "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -392,17 +400,13 @@ def main():
             "warmup": W, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": w.name, "M": w.M, "N": w.N, "K": w.K, "transA": w.transA,
-                       "transB": w.transB, "alpha": w.alpha, "beta": w.beta,
-                       "dist": {"uniform": "U[-1,1]", "normal": "N(0,1)"}[w.dist], "seed": w.seed,
-                       "injected_flips": w.n_flips, "flip_bits": [syn.BIT_LO, syn.BIT_HI],
-                       "verification_tile": [syn.TILE_M, syn.TILE_N],
-                       "parallelism": f"row-block x{world}" + (
+            "config": dict(base_config(w),
+                       parallelism= f"row-block x{world}" + (
                            (f", op(B) {args.backend.upper()} broadcast per step in {len(chunks)} column chunks "
                             f"{[c1 - c0 for c0, c1 in chunks]} overlapped with the GEMM"
                             if isinstance(chunks, list) else f", op(B) {args.backend.upper()} broadcast per step")
                            if world > 1 else ""),
-                       "l2": "no flush: operands (%.1f GiB) >> 126 MB L2" % ((d["A"].nbytes + d["B"].nbytes + d["C"].nbytes) / 2**30)},
+                       l2="no flush: operands (%.1f GiB) >> 126 MB L2" % ((d["A"].nbytes + d["B"].nbytes + d["C"].nbytes) / 2**30)),
             "fp64_peak_tflops": FP64_PEAK_TFLOPS,
             "pct_fp64_peak": 100.0 * value / (FP64_PEAK_TFLOPS * world),
             "noft_tflops": tf(ms_noft), "ft_0err_tflops": tf(ms_ft0), "ft_flips_tflops": tf(ms_ft_err),
