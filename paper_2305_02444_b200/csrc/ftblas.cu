@@ -51,7 +51,7 @@ struct Ctx {
     DevBuf hA, hB, hC;    // ftblas_dgemm_host device staging
     cudaStream_t s_up = nullptr, s_down = nullptr;  // ftblas_dgemm_host copy streams
     cudaStream_t s_side = nullptr;                   // checksum GEMM S^T (forked / joined)
-    cudaEvent_t ev_entry = nullptr, ev_exit = nullptr, ev_up[8] = {}, ev_done[16] = {}, ev_a[2] = {};
+    cudaEvent_t ev_entry = nullptr, ev_exit = nullptr, ev_up[8] = {}, ev_done[16] = {}, ev_a[4] = {};
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // cached A-side encoding (FTBLAS_REUSE_A_ENCODE)
     struct AKey {
@@ -75,7 +75,7 @@ struct Ctx {
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_exit, cudaEventDisableTiming);
         for (int q = 0; q < 8 && e == cudaSuccess; q++) e = cudaEventCreateWithFlags(&ev_up[q], cudaEventDisableTiming);
         for (int q = 0; q < 16 && e == cudaSuccess; q++) e = cudaEventCreateWithFlags(&ev_done[q], cudaEventDisableTiming);
-        for (int q = 0; q < 2 && e == cudaSuccess; q++) e = cudaEventCreateWithFlags(&ev_a[q], cudaEventDisableTiming);
+        for (int q = 0; q < 4 && e == cudaSuccess; q++) e = cudaEventCreateWithFlags(&ev_a[q], cudaEventDisableTiming);
         return e;
     }
     long long launches = 0;
@@ -603,8 +603,16 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
     // directions overlaps the DMMA work; only op(A) row block 0 and op(B) block 0 are exposed.
     const long long tiles_m = (M + FTBLAS_TILE_M - 1) / FTBLAS_TILE_M, tiles_n = (N + FTBLAS_TILE_N - 1) / FTBLAS_TILE_N;
     const long long T = tiles_m * tiles_n;
-    const long long nrb = (T / 600 >= 4 && tiles_m >= 16) ? 2 : 1;  // 2 row blocks once >= 4 waves each
-    const long long ncb = std::min<long long>(8, tiles_n);
+    // The exposed part is the upload of op(A) row block 0 + op(B) column block 0, so blocks are
+    // as square as the sizes allow; large problems use 4 x 4 blocks of >= ~7 waves each (c3:
+    // 32 x 32 tiles, 1.1 GB exposed instead of 1.3 GB with 2 x 8), smaller ones 2 x 8 / 1 x 8.
+    long long nrb, ncb;
+    if (T >= 16 * 1000 && tiles_m >= 16 && tiles_n >= 16) {
+        nrb = 4; ncb = 4;
+    } else {
+        nrb = (T / 600 >= 4 && tiles_m >= 16) ? 2 : 1;  // 2 row blocks once >= 4 waves each
+        ncb = std::min<long long>(8, tiles_n);
+    }
     auto split = [](long long tiles, long long nb, long long q, long long tile, long long lim, long long &x0,
                     long long &x1) {
         const long long per = tiles / nb, rem = tiles % nb;
