@@ -330,11 +330,13 @@ cudaError_t launch_cksum_t(const CkArgs &a, const CUtensorMap &mx, const CUtenso
 
 // Split count of a checksum GEMM with `tiles` 128-row tiles: about four waves of CTAs in
 // total, at least one BK slice per split.
-void cksum_split(long long tiles, long long K, long long &splits, long long &kper) {
+void cksum_split(long long tiles, long long K, long long Q, long long &splits, long long &kper) {
     const long long kt = std::max<long long>(1, (K + BK - 1) / BK);
-    // about 4 waves of CTAs, but every split at least 16 k-tiles deep: for small K the partial
-    // outputs (splits x P x Q doubles, written and re-read) would cost more than the DMMAs
-    splits = std::max<long long>(1, std::min<long long>({kt / 16, (4 * 148 + tiles - 1) / tiles}));
+    // about 4 waves of CTAs, but the k-split partials (splits x P x Q doubles, written and
+    // re-read) at most 1/8 of the operand bytes (P x K): c2 (Q = 128, K = 256) -> 1 split,
+    // c1 (Q = 32, K = 4096) -> 16, c3 -> 5
+    const long long cap = std::max<long long>(1, K / (8 * std::max<long long>(1, Q)));
+    splits = std::max<long long>(1, std::min<long long>({kt, cap, (4 * 148 + tiles - 1) / tiles}));
     kper = (kt + splits - 1) / splits * BK;
     splits = (K + kper - 1) / kper;
 }
@@ -427,8 +429,8 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
         const bool pre = c.checksum_mode == FTBLAS_CHECKSUM_GEMM;
         long long spR = 1, kpR = Kp, spS = 1, kpS = Kp;
         if (pre) {
-            cksum_split(ntm * ((ntn + 127) / 128), K, spR, kpR);
-            cksum_split(ntn * ((ntm + 127) / 128), K, spS, kpS);
+            cksum_split(ntm * ((ntn + 127) / 128), K, std::min<long long>(ntn, 128), spR, kpR);
+            cksum_split(ntn * ((ntm + 127) / 128), K, std::min<long long>(ntm, 128), spS, kpS);
         }
         // workspace: A side first (VA, lineA, tmaxA: independent of N, so a chunked caller can
         // reuse them), then the B side, then the checksum-GEMM partials
