@@ -368,52 +368,58 @@ __device__ void encode_mn_contig(const EncodeOperand &o, const EncodeArgs &a, in
 
 // k contiguous (op(A) = A 'T', op(B) = B 'N'): thread owns k = kbeg + tid + 256q and loops over
 // the 128 mn of the tile (each load instruction of a warp reads 256 contiguous bytes).  The
-// per-mn |.| sums over the warp's 32 k are formed by a transposing butterfly (31 shuffles per
-// 32 mn instead of 160): afterwards lane l holds the sum for mn = 32g + l.
+// per-mn |.| sums over the warp's 32 k are formed 16 mn at a time by a transposing butterfly
+// (15 + 1 shuffles per 16 mn instead of 80): afterwards lanes 2j, 2j+1 hold the sum for
+// mn = 16 g + j.  16-wide groups keep the kernel at <= 80 registers (3 blocks per SM: the
+// encode is a latency-bound HBM stream, more loads in flight is what it needs).
 __device__ void encode_k_contig(const EncodeOperand &o, const EncodeArgs &a, int t, long long kbeg,
                                 long long kend, double *red, double &tm) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long i0 = (long long)t * 128;
     const int nrow = (int)min(128ll, o.MNd - i0);
-    double la[4] = {0.0, 0.0, 0.0, 0.0};
+    double la[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     for (long long k = kbeg + tid; k - tid < kend; k += NTHREADS) {
         const bool kv = k < kend && k < a.K;
         const double *row0 = o.X + k + i0 * o.ld;
         double s = 0.0, sa = 0.0;
 #pragma unroll
-        for (int g = 0; g < 4; g++) {
-            double v[32];
+        for (int g = 0; g < 8; g++) {
+            double v[16];
 #pragma unroll
-            for (int j = 0; j < 32; j++) {
-                const int i = g * 32 + j;
+            for (int j = 0; j < 16; j++) {
+                const int i = g * 16 + j;
                 const double x = (kv && i < nrow) ? __ldcs(row0 + (long long)i * o.ld) : 0.0;
                 s += x;
                 v[j] = fabs(x);
             }
 #pragma unroll
-            for (int j = 0; j < 32; j++) sa += v[j];
+            for (int j = 0; j < 16; j++) sa += v[j];
 #pragma unroll
-            for (int off = 16; off; off >>= 1) {
+            for (int off = 16; off >= 2; off >>= 1) {
                 const bool up = (lane & off) != 0;
 #pragma unroll
-                for (int j = 0; j < off; j++) {
-                    const double send = up ? v[j] : v[j + off];
-                    const double keep = up ? v[j + off] : v[j];
+                for (int j = 0; j < off / 2; j++) {
+                    const double send = up ? v[j] : v[j + off / 2];
+                    const double keep = up ? v[j + off / 2] : v[j];
                     v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
                 }
             }
-            la[g] += v[0];
+            la[g] += v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
         }
         if (k < kend) {
             o.V[(long long)t * a.Kp + k] = s;  // 0 for k >= K
             tm = fmax(tm, sa);
         }
     }
+    // lane l holds mn = 16 g + idx(l), idx = 8 b4 + 4 b3 + 2 b2 + b1; even lanes write
+    if ((lane & 1) == 0) {
+        const int idx = ((lane >> 1) & 1) + ((lane >> 2) & 1) * 2 + ((lane >> 3) & 1) * 4 + ((lane >> 4) & 1) * 8;
 #pragma unroll
-    for (int g = 0; g < 4; g++) red[warp * 128 + g * 32 + lane] = la[g];
+        for (int g = 0; g < 8; g++) red[warp * 128 + g * 16 + idx] = la[g];
+    }
 }
 
-__global__ void __launch_bounds__(NTHREADS) encode_kernel(EncodeArgs a) {
+__global__ void __launch_bounds__(NTHREADS, 3) encode_kernel(EncodeArgs a) {
     __shared__ double red[(NTHREADS / 32) * 128];
     __shared__ double wmax[NTHREADS / 32];
     const EncodeOperand &o = a.op[blockIdx.z];
