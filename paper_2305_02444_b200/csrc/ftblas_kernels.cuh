@@ -347,18 +347,36 @@ __device__ void encode_mn_contig(const EncodeOperand &o, const EncodeArgs &a, in
                 for (int r = 0; r < 4; r++) x[u][r] = (kv && rv[r]) ? __ldcs(col + rows[r]) : 0.0;
             }
         }
+        // v[u] = this lane's part of the sum of column u, v[U + u] of its |.| sum; the 2U = 8
+        // warp sums by a transposing butterfly (7 + 2 shuffles instead of 40): afterwards lane
+        // l holds value 4 b4 + 2 b3 + b2 (b = bits of l), the same in the 4 lanes l ^ {1,2,3}
+        double v[2 * U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            const long long kk = k + 8 * u;
-            double s = (x[u][0] + x[u][1]) + (x[u][2] + x[u][3]);
-            double sa = (fabs(x[u][0]) + fabs(x[u][1])) + (fabs(x[u][2]) + fabs(x[u][3]));
+            v[u] = (x[u][0] + x[u][1]) + (x[u][2] + x[u][3]);
+            v[U + u] = (fabs(x[u][0]) + fabs(x[u][1])) + (fabs(x[u][2]) + fabs(x[u][3]));
 #pragma unroll
             for (int r = 0; r < 4; r++) la[r] += fabs(x[u][r]);
-            s = warp_sum(s);
-            sa = warp_sum(sa);
-            if (kk < kend) {
-                if (lane == 0) o.V[(long long)t * a.Kp + kk] = s;  // 0 for kk >= K
-                tm = fmax(tm, sa);
+        }
+#pragma unroll
+        for (int off = 16; off >= 4; off >>= 1) {
+            const bool up = (lane & off) != 0;
+#pragma unroll
+            for (int j = 0; j < off / 4; j++) {
+                const double send = up ? v[j] : v[j + off / 4];
+                const double keep = up ? v[j + off / 4] : v[j];
+                v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+        }
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+        const int idx = ((lane >> 2) & 1) + ((lane >> 3) & 1) * 2 + ((lane >> 4) & 1) * 4;
+        const long long kk = k + 8 * (idx & (U - 1));
+        if (kk < kend) {
+            if (idx < U) {
+                if ((lane & 3) == 0) o.V[(long long)t * a.Kp + kk] = v[0];  // 0 for kk >= K
+            } else {
+                tm = fmax(tm, v[0]);
             }
         }
     }
