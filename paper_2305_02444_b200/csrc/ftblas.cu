@@ -477,13 +477,33 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
         ea.op[1] = opB;
         ea.K = (alpha == 0.0) ? 0 : K;  // alpha == 0: A, B are not read (encodes are zero)
         ea.Kp = Kp; ea.kper = kper; ea.kch = kch; ea.rep = append ? nullptr : g.rep;
-        dim3 grid((unsigned)(skip_a ? ntn : std::max(ntm, ntn)), (unsigned)kch, skip_a ? 1 : 2);
-        encode_kernel<<<grid, NTHREADS, 0, c.stream>>>(ea);
+        // one launch per layout path (encode_kernel<PATH>): both operands in one launch when
+        // they share it; the first launch zeroes the report
+        {
+            const int nops = skip_a ? 1 : 2;
+            auto path_of = [](const EncodeOperand &o) { return o.kc ? 0 : (o.vec ? 1 : 2); };
+            ReportHdr *rep0 = ea.rep;
+            for (int b0 = 0; b0 < nops;) {
+                int b1 = b0 + 1;
+                while (b1 < nops && path_of(ea.op[b1]) == path_of(ea.op[b0])) b1++;
+                long long tiles = 0;
+                for (int q = b0; q < b1; q++) tiles = std::max<long long>(tiles, ea.op[q].ntiles);
+                ea.op_base = b0;
+                ea.rep = b0 == 0 ? rep0 : nullptr;
+                const dim3 grid((unsigned)tiles, (unsigned)kch, (unsigned)(b1 - b0));
+                switch (path_of(ea.op[b0])) {
+                    case 0: encode_kernel<0><<<grid, NTHREADS, 0, c.stream>>>(ea); break;
+                    case 1: encode_kernel<1><<<grid, NTHREADS, 0, c.stream>>>(ea); break;
+                    default: encode_kernel<2><<<grid, NTHREADS, 0, c.stream>>>(ea); break;
+                }
+                c.launches++;
+                CK(cudaGetLastError(), "encode_kernel launch");
+                b0 = b1;
+            }
+        }
         if (!skip_a) {
             c.a_valid = true; c.a_key = akey; c.a_kch = kch; c.a_ws_gen = c.ws_gen;
         }
-        c.launches++;
-        CK(cudaGetLastError(), "encode_kernel launch");
         if (pre && K > 0 && alpha != 0.0) {
             // checksum GEMMs (the border of C^f = A^c B^r) on the FP64
             // tensor cores:  R (M x ntn, ld M)   = op(A) . WB^T   [WB^T: k x ntn, 'N', ld Kp]

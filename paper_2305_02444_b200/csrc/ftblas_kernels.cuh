@@ -301,6 +301,7 @@ struct EncodeArgs {
     long long K, Kp, kper;
     int kch;
     ReportHdr *rep;  // zeroed here (stream-ordered before the GEMM kernel)
+    int op_base;     // operand of blockIdx.z = 0
 };
 
 // an unsigned stored in the low word of a double's bit pattern (smem / DSMEM transport only)
@@ -384,63 +385,82 @@ __device__ void encode_mn_contig(const EncodeOperand &o, const EncodeArgs &a, in
     for (int r = 0; r < 4; r++) red[warp * 128 + rows[r]] = la[r];
 }
 
-// k contiguous (op(A) = A 'T', op(B) = B 'N'): thread owns k = kbeg + tid + 256q and loops over
-// the 128 mn of the tile (each load instruction of a warp reads 256 contiguous bytes).  The
-// per-mn |.| sums over the warp's 32 k are formed 16 mn at a time by a transposing butterfly
-// (15 + 1 shuffles per 16 mn instead of 80): afterwards lanes 2j, 2j+1 hold the sum for
-// mn = 16 g + j.  16-wide groups keep the kernel at <= 80 registers (3 blocks per SM: the
-// encode is a latency-bound HBM stream, more loads in flight is what it needs).
+// k contiguous (op(A) = A 'T', op(B) = B 'N'): the chunk is walked in slabs of 128 k; warp w
+// owns mn 16w .. 16w+15 of the tile and lane l the 4 consecutive k 4l .. 4l+3 of the slab, so
+// one warp-wide load pair reads 1 KB of one mn (2 x 16 B per lane when 16-byte aligned).  The
+// per-mn |.| sums over the slab's 128 k: transposing butterfly over the warp's 16 mn (15 + 1
+// shuffles), lanes 2j, 2j+1 then hold mn 16w + j.  The per-k sums over the tile's 128 mn (V and
+// the |.| sums behind tmax) are combined across the 8 warps through shared memory in warp order.
 __device__ void encode_k_contig(const EncodeOperand &o, const EncodeArgs &a, int t, long long kbeg,
                                 long long kend, double *red, double &tm) {
+    __shared__ double ks[NTHREADS / 32][2][128];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long i0 = (long long)t * 128;
     const int nrow = (int)min(128ll, o.MNd - i0);
-    double la[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    for (long long k = kbeg + tid; k - tid < kend; k += NTHREADS) {
-        const bool kv = k < kend && k < a.K;
-        const double *row0 = o.X + k + i0 * o.ld;
-        double s = 0.0, sa = 0.0;
+    const long long klim = min(kend, a.K);
+    const int idx = ((lane >> 1) & 1) + ((lane >> 2) & 1) * 2 + ((lane >> 3) & 1) * 4 + ((lane >> 4) & 1) * 8;
+    double la = 0.0;
+    for (long long k0 = kbeg; k0 < kend; k0 += 128) {
+        const long long k = k0 + 4 * lane;
+        const bool full = o.vec && k + 3 < klim;  // 2 x 16-byte loads
+        double s4[4] = {0.0, 0.0, 0.0, 0.0}, sa4[4] = {0.0, 0.0, 0.0, 0.0}, v[16];
 #pragma unroll
-        for (int g = 0; g < 8; g++) {
-            double v[16];
+        for (int j = 0; j < 16; j++) {
+            const int i = warp * 16 + j;
+            double x[4] = {0.0, 0.0, 0.0, 0.0};
+            if (i < nrow) {
+                const double *p = o.X + k + (i0 + i) * o.ld;
+                if (full) {
+                    const double2 u0 = __ldcs(reinterpret_cast<const double2 *>(p));
+                    const double2 u1 = __ldcs(reinterpret_cast<const double2 *>(p) + 1);
+                    x[0] = u0.x; x[1] = u0.y; x[2] = u1.x; x[3] = u1.y;
+                } else {
 #pragma unroll
-            for (int j = 0; j < 16; j++) {
-                const int i = g * 16 + j;
-                const double x = (kv && i < nrow) ? __ldcs(row0 + (long long)i * o.ld) : 0.0;
-                s += x;
-                v[j] = fabs(x);
-            }
-#pragma unroll
-            for (int j = 0; j < 16; j++) sa += v[j];
-#pragma unroll
-            for (int off = 16; off >= 2; off >>= 1) {
-                const bool up = (lane & off) != 0;
-#pragma unroll
-                for (int j = 0; j < off / 2; j++) {
-                    const double send = up ? v[j] : v[j + off / 2];
-                    const double keep = up ? v[j + off / 2] : v[j];
-                    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                    for (int q = 0; q < 4; q++) x[q] = (k + q < klim) ? __ldcs(p + q) : 0.0;
                 }
             }
-            la[g] += v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
-        }
-        if (k < kend) {
-            o.V[(long long)t * a.Kp + k] = s;  // 0 for k >= K
-            tm = fmax(tm, sa);
-        }
-    }
-    // lane l holds mn = 16 g + idx(l), idx = 8 b4 + 4 b3 + 2 b2 + b1; even lanes write
-    if ((lane & 1) == 0) {
-        const int idx = ((lane >> 1) & 1) + ((lane >> 2) & 1) * 2 + ((lane >> 3) & 1) * 4 + ((lane >> 4) & 1) * 8;
 #pragma unroll
-        for (int g = 0; g < 8; g++) red[warp * 128 + g * 16 + idx] = la[g];
+            for (int q = 0; q < 4; q++) { s4[q] += x[q]; sa4[q] += fabs(x[q]); }
+            v[j] = (fabs(x[0]) + fabs(x[1])) + (fabs(x[2]) + fabs(x[3]));
+        }
+#pragma unroll
+        for (int off = 16; off >= 2; off >>= 1) {
+            const bool up = (lane & off) != 0;
+#pragma unroll
+            for (int j = 0; j < off / 2; j++) {
+                const double send = up ? v[j] : v[j + off / 2];
+                const double keep = up ? v[j + off / 2] : v[j];
+                v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+        }
+        la += v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+#pragma unroll
+        for (int q = 0; q < 4; q++) { ks[warp][0][4 * lane + q] = s4[q]; ks[warp][1][4 * lane + q] = sa4[q]; }
+        __syncthreads();
+        if (tid < 128 && k0 + tid < kend) {
+            double sv = 0.0, sav = 0.0;
+#pragma unroll
+            for (int w = 0; w < NTHREADS / 32; w++) { sv += ks[w][0][tid]; sav += ks[w][1][tid]; }
+            o.V[(long long)t * a.Kp + k0 + tid] = sv;  // 0 for k >= K
+            tm = fmax(tm, sav);
+        }
+        __syncthreads();
     }
+    // line partials: this warp's 16 mn, zeros elsewhere (the caller adds the warps' rows)
+    for (int i = lane; i < 128; i += 32) red[warp * 128 + i] = 0.0;
+    __syncwarp();
+    if ((lane & 1) == 0) red[warp * 128 + warp * 16 + idx] = la;
 }
 
+// PATH 0: k contiguous (slab walk, cross-warp k sums in shared memory);
+// PATH 1 / 2: mn contiguous with 16-byte / 8-byte loads.  3 blocks / SM (<= 80 registers): a
+// latency-bound stream that wants loads in flight).  Operand = a.op[a.op_base + blockIdx.z];
+// the host launches once per layout path (once in total when both operands share it).
+template <int PATH>
 __global__ void __launch_bounds__(NTHREADS, 3) encode_kernel(EncodeArgs a) {
     __shared__ double red[(NTHREADS / 32) * 128];
     __shared__ double wmax[NTHREADS / 32];
-    const EncodeOperand &o = a.op[blockIdx.z];
+    const EncodeOperand &o = a.op[a.op_base + blockIdx.z];
     const int t = blockIdx.x, ch = blockIdx.y, tid = threadIdx.x;
     if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0 && a.rep) {
         a.rep->count = 0; a.rep->tiles_flagged = 0; a.rep->rows_flagged = 0; a.rep->cols_flagged = 0;
@@ -449,9 +469,9 @@ __global__ void __launch_bounds__(NTHREADS, 3) encode_kernel(EncodeArgs a) {
     const long long kbeg = (long long)ch * a.kper;
     const long long kend = min(kbeg + a.kper, a.Kp);
     double tm = 0.0;
-    if (o.kc)       encode_k_contig(o, a, t, kbeg, kend, red, tm);
-    else if (o.vec) encode_mn_contig<true>(o, a, t, kbeg, kend, red, tm);
-    else            encode_mn_contig<false>(o, a, t, kbeg, kend, red, tm);
+    if (PATH == 0)      encode_k_contig(o, a, t, kbeg, kend, red, tm);
+    else if (PATH == 1) encode_mn_contig<true>(o, a, t, kbeg, kend, red, tm);
+    else                encode_mn_contig<false>(o, a, t, kbeg, kend, red, tm);
 #pragma unroll
     for (int off = 16; off; off >>= 1) tm = fmax(tm, __shfl_xor_sync(0xffffffffu, tm, off));
     if ((tid & 31) == 0) wmax[tid >> 5] = tm;
