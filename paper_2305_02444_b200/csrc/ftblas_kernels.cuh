@@ -15,10 +15,11 @@
 //                   (lines 517, 540, 521) before the store.  FT=false is the non-FT
 //                   baseline (same tiles/mainloop).
 //
-// CTA: MMA warps in a 2 (M) x NWN (N) grid, warp tile 64 x 32 = 8 x 4 DMMA fragments of 8x8,
-// BK = 32, plus one producer warpgroup.  NWN = 4: 128 x 128 CTA tile, one CTA per SM, 3-stage
-// ring.  NWN = 2 ("pair"): 128 x 64 CTA tile, two CTAs per SM, 2-stage ring; in FT mode the
-// two halves of a 128 x 128 verification tile are a cluster exchanging row sums through DSMEM.
+// CTA: 8 MMA warps (DMMA fragments of 8x8, BK = 32) plus producer threads (struct Warps).
+// NWN = 4: 128 x 128 CTA tile, 2 x 4 warps of 64 x 32, producer warpgroup, one CTA per SM,
+// 3-stage ring.  NWN = 2 ("pair"): 128 x 64 CTA tile, 4 x 2 warps of 32 x 32, one producer
+// warp, two CTAs per SM, 2-stage ring; in FT mode the two halves of a 128 x 128 verification
+// tile are a cluster exchanging row sums through DSMEM.
 //   side_finalize_kernel / cksum_kernel: see their sections.  DESIGN.md section 5.
 #pragma once
 #include <cstdint>
@@ -592,7 +593,7 @@ __device__ void warp_recompute(const GemmArgs &g, long long i, long long j, doub
     }
 }
 
-// Block = NTHREADS MMA threads (8 warps) + a producer warpgroup.  Thread 0 of the producer
+// Block = NTHREADS MMA threads (8 warps) + producer threads (Warps<NWN>::PT).  Thread 0 of the producer
 // issues the TMA boxes of each stage (and the bulk copies of the checksum-vector slices) and
 // arms the stage's `full` mbarrier with the byte count; MMA warps release stages through
 // `empty` mbarriers (no CTA-wide barrier in the mainloop).  The other producer threads only
