@@ -417,3 +417,25 @@ def test_many_faulted_tiles_leave_neighbours_clean(tB, tiles):
     finally:
         ft.ftblas_clear_fault_plan()
         ft.ftblas_set_tile_policy("auto")
+
+
+def test_host_entry_4x4_blocks_bitwise_equal_device():
+    """The e2e entry at a size that takes the 4 x 4 block pipeline (16384^2 x 4096, beta != 0 so
+    C0 blocks are uploaded too, 200 flips): C and the report equal the single device call's
+    bitwise (blocks are whole 128 x 128 tiles, so every tile does the same arithmetic)."""
+    import torch
+    ft = _lib("gemm")
+    w = syn.Workload("hb4", 16384, 16384, 4096, "N", "N", 1.0, 0.5, "uniform", True, seed=41, n_flips=200)
+    d = syn.make_inputs(w)
+    plan = syn.fault_plan(w.M, w.N, w.n_flips, w.seed)
+    C_dev, rep_dev = run_gpu(ft, w, d, plan=plan)
+    ft.ftblas_set_fault_plan(*plan)
+    C = np.asfortranarray(d["C"].copy())
+    rep = ft.Report(512)
+    ft.ftblas_dgemm_host(w.transA, w.transB, w.M, w.N, w.K, w.alpha, np.asfortranarray(d["A"]),
+                         d["lda"], np.asfortranarray(d["B"]), d["ldb"], w.beta, C, d["ldc"], rep)
+    ft.ftblas_clear_fault_plan()
+    torch.cuda.synchronize()
+    assert rep.count == rep_dev.count == w.n_flips
+    assert report_key(rep.entries()) == report_key(rep_dev.entries())
+    assert np.array_equal(C, C_dev)
