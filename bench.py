@@ -367,9 +367,10 @@ def main():
         e2e_step()
         ms_e2e = timed(e2e_step, max(2, min(K, 3)))
         # the last step's report (accumulated over the pipeline's blocks): every flip located
-        rep_e2e = fb.ftblas_report_fetch(fb.Report(max(16, 2 * len(plan_loc[0]))))
+        n_loc = 0 if plan_loc is None else len(plan_loc[0])
+        rep_e2e = fb.ftblas_report_fetch(fb.Report(max(16, 2 * n_loc)))
         got_e2e = sorted((e["i"], e["j"]) for e in rep_e2e.entries())
-        want_e2e = sorted(zip(plan_loc[0].tolist(), plan_loc[1].tolist()))
+        want_e2e = [] if plan_loc is None else sorted(zip(plan_loc[0].tolist(), plan_loc[1].tolist()))
         e2e_ok = sum_over_ranks(0.0 if (rep_e2e.count == len(want_e2e) and got_e2e == want_e2e) else 1.0) == 0.0
         fb.ftblas_clear_fault_plan()
         e2e = {"value": flops_total / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
