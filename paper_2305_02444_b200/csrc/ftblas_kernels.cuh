@@ -1232,8 +1232,9 @@ __global__ void __launch_bounds__(256) side_finalize_kernel(FinArgs f) {
 // vectors (k-contiguous, ld Kp).  A CTA computes 128 rows of P times all QN (>= Q) columns
 // over one k-split; split s writes its partial to out + s * split_stride (no atomics: the
 // FT_PRE epilogue adds the splits in order, so the result is deterministic).  Same producer /
-// TMA / swizzled-fragment machinery as gemm_kernel; warp w owns rows 16w..16w+15 (2 DMMA
-// row fragments) x QN/8 column fragments.
+// TMA / swizzled-fragment machinery as gemm_kernel; the 8 MMA warps form NWM x NWN with
+// NWN = QN / 32 (at least 1), so QN = 128 runs the main kernel's 64 x 32 warp tiles (12
+// fragment loads per 32 DMMA), QN = 64 32 x 32, QN <= 32 16 x QN.
 struct CkArgs {
     const double *X, *Y;
     long long ldx, ldy;
@@ -1253,11 +1254,14 @@ template <bool KCX, bool TMA, int QN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     cksum_kernel(const __grid_constant__ CkArgs g, const __grid_constant__ CUtensorMap tmX,
                  const __grid_constant__ CUtensorMap tmY) {
-    constexpr int FQ = QN / 8;
+    constexpr int NWN_C = QN >= 32 ? QN / 32 : 1, NWM_C = 8 / NWN_C;
+    constexpr int WM_C = BM / NWM_C, WN_C = QN / NWN_C;
+    constexpr int FMC = WM_C / 8, FQ = WN_C / 8;
     extern __shared__ __align__(1024) double smem_raw[];
     __shared__ __align__(8) unsigned long long full_bar[STAGES], empty_bar[STAGES];
     double *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) / 8u;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp % NWM_C, wn = warp / NWM_C;
     const long long p0 = (long long)blockIdx.x * BM;
     const long long kbeg = (long long)blockIdx.y * g.kper;
     const long long kend = min(g.K, kbeg + g.kper);
@@ -1290,25 +1294,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         return;
     }
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(MMA_REGS));
-    double acc[2][FQ][2];
+    double acc[FMC][FQ][2];
 #pragma unroll
-    for (int a = 0; a < 2; a++)
+    for (int a = 0; a < FMC; a++)
 #pragma unroll
         for (int b = 0; b < FQ; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
-    const FragAddr<KCX> fX(warp * 16, lane);
-    const FragAddr<true, QN> fY(0, lane);
+    const FragAddr<KCX> fX(wm * WM_C, lane);
+    const FragAddr<true, QN> fY(wn * WN_C, lane);
     auto consume = [&](const int st, const int kt) {
         mbar_wait(&full_bar[st], (kt / STAGES) & 1);
         const double *x_s = sX(st), *y_s = sY(st);
 #pragma unroll
         for (int kk = 0; kk < BK / 4; kk++) {
-            double xf[2], yf[FQ];
+            double xf[FMC], yf[FQ];
 #pragma unroll
-            for (int f = 0; f < 2; f++) xf[f] = x_s[fX(f, kk)];
+            for (int f = 0; f < FMC; f++) xf[f] = x_s[fX(f, kk)];
 #pragma unroll
             for (int f = 0; f < FQ; f++) yf[f] = y_s[fY(f, kk)];
 #pragma unroll
-            for (int a = 0; a < 2; a++)
+            for (int a = 0; a < FMC; a++)
 #pragma unroll
                 for (int b = 0; b < FQ; b++) dmma(acc[a][b][0], acc[a][b][1], xf[a], yf[b]);
         }
@@ -1322,13 +1326,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     double *out = g.out + (long long)blockIdx.y * g.split_stride;
 #pragma unroll
-    for (int a = 0; a < 2; a++) {
-        const long long pi = p0 + frag_mn<KCX>(warp * 16, a, lane >> 2);
+    for (int a = 0; a < FMC; a++) {
+        const long long pi = p0 + frag_mn<KCX>(wm * WM_C, a, lane >> 2);
 #pragma unroll
         for (int b = 0; b < FQ; b++)
 #pragma unroll
             for (int e = 0; e < 2; e++) {
-                const long long q = frag_mn<true>(0, b, 2 * (lane & 3) + e);
+                const long long q = frag_mn<true>(wn * WN_C, b, 2 * (lane & 3) + e);
                 if (pi < g.P && q < g.Q) out[pi + q * g.ldo] = acc[a][b][e];
             }
     }
