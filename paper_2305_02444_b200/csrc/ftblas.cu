@@ -380,7 +380,7 @@ cudaError_t cksum_gemm(bool kcx, const double *X, long long ldx, long long P, co
 int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K, double alpha,
                const double *A, long long lda, const double *B, long long ldb, double beta, double *C,
                long long ldc, ftblas_err_report *rep, long long off_i = 0, long long off_j = 0,
-               bool append = false, bool reuse_a = false) {
+               bool append = false, bool reuse_a = false, bool inject = true) {
     static_assert(sizeof(Correction) == sizeof(ftblas_correction), "ABI");
     Ctx &c = ctx();
     int rc = check_args(ta, tb, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta);
@@ -470,6 +470,7 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
         g.off_i = off_i; g.off_j = off_j;
         rc = prepare_plan(M, N, off_i, off_j, g);
         if (rc) return rc;
+        if (!inject) { g.plan_ptr = nullptr; g.plan_i = nullptr; g.plan_j = nullptr; g.plan_bit = nullptr; }
         EncodeArgs ea{};
         const EncodeOperand opA{A, lda, M, kca ? 1 : 0, va ? 1 : 0, const_cast<double *>(g.VA), lineA, tmaxA, (int)ntm};
         const EncodeOperand opB{B, ldb, N, kcb ? 1 : 0, vb ? 1 : 0, const_cast<double *>(g.WB), lineB, tmaxB, (int)ntn};
@@ -662,12 +663,46 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
         return cudaMemcpy2DAsync(dC + r0 + c0 * dlc, dlc * 8, C + r0 + c0 * ldc, ldc * 8, (r1 - r0) * 8, c1 - c0,
                                  cudaMemcpyHostToDevice, c.s_up);
     };
-    CK(up_A(0), "H2D A");
+    // Block (0, 0) in two k halves when K is deep (4 x 4 pipelines, K >= 8192): the first
+    // call needs only half of op(A) row block 0 and op(B) column block 0, which halves the
+    // exposed upload; the second accumulates onto it (beta = 1) and carries the fault plan, so
+    // reports are those of the one-call block.  ev_up[7] marks the first halves.
+    const bool ksplit = readAB && nrb == 4 && ncb <= 7 && K >= 8192;
+    const long long K1 = ksplit ? (K / 2) / BK * BK : K;
+    auto up_A_k = [&](long long rb, long long k0, long long k1) -> cudaError_t {
+        long long r0, r1;
+        split(tiles_m, nrb, rb, FTBLAS_TILE_M, M, r0, r1);
+        if (is_t(transA))  // op(A)(r0:r1, k0:k1) = rows k0..k1 of columns r0..r1 of the K x M stored A
+            return cudaMemcpy2DAsync(dA + r0 * dla + k0, dla * 8, A + r0 * lda + k0, lda * 8, (k1 - k0) * 8, r1 - r0,
+                                     cudaMemcpyHostToDevice, c.s_up);
+        return cudaMemcpy2DAsync(dA + r0 + k0 * dla, dla * 8, A + r0 + k0 * lda, lda * 8, (r1 - r0) * 8, k1 - k0,
+                                 cudaMemcpyHostToDevice, c.s_up);
+    };
+    auto up_B_k = [&](long long cb, long long k0, long long k1) -> cudaError_t {
+        long long c0, c1;
+        split(tiles_n, ncb, cb, FTBLAS_TILE_N, N, c0, c1);
+        if (is_t(transB))  // op(B)(k0:k1, c0:c1) = columns k0..k1 of rows c0..c1 of the N x K stored B
+            return cudaMemcpy2DAsync(dB + c0 + k0 * dlb, dlb * 8, B + c0 + k0 * ldb, ldb * 8, (c1 - c0) * 8, k1 - k0,
+                                     cudaMemcpyHostToDevice, c.s_up);
+        return cudaMemcpy2DAsync(dB + c0 * dlb + k0, dlb * 8, B + c0 * ldb + k0, ldb * 8, (k1 - k0) * 8, c1 - c0,
+                                 cudaMemcpyHostToDevice, c.s_up);
+    };
+    if (ksplit) {
+        CK(up_A_k(0, 0, K1), "H2D A");
+        CK(up_B_k(0, 0, K1), "H2D B");
+        CK(up_C0(0, 0), "H2D C");
+        CK(cudaEventRecord(c.ev_up[7], c.s_up), "event");
+        CK(up_A_k(0, K1, K), "H2D A");
+    } else {
+        CK(up_A(0), "H2D A");
+    }
     CK(cudaEventRecord(c.ev_a[0], c.s_up), "event");
     for (long long cb = 0; cb < ncb; cb++) {
         long long c0, c1;
         split(tiles_n, ncb, cb, FTBLAS_TILE_N, N, c0, c1);
-        if (readAB) {
+        if (ksplit && cb == 0) {
+            CK(up_B_k(0, K1, K), "H2D B");
+        } else if (readAB) {
             if (is_t(transB))  // op(B)(:, c0:c1) = rows c0..c1 of the N x K stored B
                 CK(cudaMemcpy2DAsync(dB + c0, dlb * 8, B + c0, ldb * 8, (c1 - c0) * 8, K, cudaMemcpyHostToDevice,
                                      c.s_up), "H2D B");
@@ -675,13 +710,25 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
                 CK(cudaMemcpy2DAsync(dB + c0 * dlb, dlb * 8, B + c0 * ldb, ldb * 8, K * 8, c1 - c0,
                                      cudaMemcpyHostToDevice, c.s_up), "H2D B");
         }
-        CK(up_C0(0, cb), "H2D C");
+        if (!(ksplit && cb == 0)) CK(up_C0(0, cb), "H2D C");
         CK(cudaEventRecord(c.ev_up[cb], c.s_up), "event");
     }
     for (long long rb = 1; rb < nrb; rb++) {
         CK(up_A(rb), "H2D A");
         for (long long cb = 0; cb < ncb; cb++) CK(up_C0(rb, cb), "H2D C");
         CK(cudaEventRecord(c.ev_a[rb], c.s_up), "event");
+    }
+    if (ksplit) {  // first k half of block (0, 0): no fault injection, report reset
+        long long c0, c1;
+        split(tiles_n, ncb, 0, FTBLAS_TILE_N, N, c0, c1);
+        long long r0, r1;
+        split(tiles_m, nrb, 0, FTBLAS_TILE_M, M, r0, r1);
+        CK(cudaStreamWaitEvent(c.stream, c.ev_up[7], 0), "wait");
+        const double *Ab = is_t(transA) ? dA + r0 * dla : dA + r0;
+        const double *Bb = is_t(transB) ? dB + c0 : dB + c0 * dlb;
+        rc = dgemm_impl(true, transA, transB, r1 - r0, c1 - c0, K1, alpha, Ab, dla, Bb, dlb, beta, dC + r0 + c0 * dlc,
+                        dlc, nullptr, r0, c0, false, false, false);
+        if (rc) return rc;
     }
     for (long long rb = 0; rb < nrb; rb++) {
         long long r0, r1;
@@ -694,9 +741,16 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
             if (rb == 0) CK(cudaStreamWaitEvent(c.stream, c.ev_up[cb], 0), "wait");
             const double *Bb = readAB ? (is_t(transB) ? dB + c0 : dB + c0 * dlb) : nullptr;
             const bool first = rb == 0 && cb == 0;
-            rc = dgemm_impl(true, transA, transB, r1 - r0, c1 - c0, K, alpha, Ab, readAB ? dla : std::max<long long>(1, ar),
-                            Bb, readAB ? dlb : std::max<long long>(1, br), beta, dC + r0 + c0 * dlc, dlc, nullptr, r0,
-                            c0, !first, cb > 0);
+            if (first && ksplit) {  // second k half of block (0, 0) onto the first (beta = 1)
+                const double *Ak = is_t(transA) ? Ab + K1 : Ab + K1 * dla;
+                const double *Bk = is_t(transB) ? Bb + K1 * dlb : Bb + K1;
+                rc = dgemm_impl(true, transA, transB, r1 - r0, c1 - c0, K - K1, alpha, Ak, dla, Bk, dlb, 1.0,
+                                dC + r0 + c0 * dlc, dlc, nullptr, r0, c0, true, false);
+            } else {
+                rc = dgemm_impl(true, transA, transB, r1 - r0, c1 - c0, K, alpha, Ab,
+                                readAB ? dla : std::max<long long>(1, ar), Bb, readAB ? dlb : std::max<long long>(1, br),
+                                beta, dC + r0 + c0 * dlc, dlc, nullptr, r0, c0, !first, cb > 0);
+            }
             if (rc) return rc;
             const int q = (int)(rb * ncb + cb);
             CK(cudaEventRecord(c.ev_done[q], c.stream), "event");

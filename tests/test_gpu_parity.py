@@ -439,3 +439,35 @@ def test_host_entry_4x4_blocks_bitwise_equal_device():
     assert rep.count == rep_dev.count == w.n_flips
     assert report_key(rep.entries()) == report_key(rep_dev.entries())
     assert np.array_equal(C, C_dev)
+
+
+@pytest.mark.parametrize("tA,tB", [("N", "N"), ("T", "T")])
+def test_host_entry_ksplit_first_block(tA, tB):
+    """The e2e entry at a depth that splits pipeline block (0, 0) into two k halves
+    (16384^2 x 8192, 4 x 4 blocks, beta != 0, 150 flips, both transposes): same report as the
+    single device call, C within the elementwise bound of it (the split block sums in another
+    order; every other block is bitwise equal)."""
+    import torch
+    ft = _lib("gemm")
+    w = syn.Workload("hb5", 16384, 16384, 8192, tA, tB, 1.25, -0.5, "uniform", True, seed=43, n_flips=150)
+    d = syn.make_inputs(w)
+    plan = syn.fault_plan(w.M, w.N, w.n_flips, w.seed)
+    C_dev, rep_dev = run_gpu(ft, w, d, plan=plan)
+    ft.ftblas_set_fault_plan(*plan)
+    C = np.asfortranarray(d["C"].copy())
+    rep = ft.Report(512)
+    ft.ftblas_dgemm_host(w.transA, w.transB, w.M, w.N, w.K, w.alpha, np.asfortranarray(d["A"]),
+                         d["lda"], np.asfortranarray(d["B"]), d["ldb"], w.beta, C, d["ldc"], rep)
+    ft.ftblas_clear_fault_plan()
+    torch.cuda.synchronize()
+    assert rep.count == rep_dev.count == w.n_flips
+    assert report_key(rep.entries()) == report_key(rep_dev.entries())
+    # block (0, 0) of the 4 x 4 pipeline: rows / cols [0, 4096); everything else bitwise
+    outside = np.ones(C.shape, dtype=bool)
+    outside[:4096, :4096] = False
+    assert np.array_equal(C[outside], C_dev[outside])
+    opA = d["A"] if tA == "N" else d["A"].T
+    opB = d["B"] if tB == "N" else d["B"].T
+    ab = np.abs(opA[:4096, :]) @ np.abs(opB[:, :4096])
+    tol = gemm_bound(w.K, w.alpha, w.beta, ab, np.abs(d["C"][:4096, :4096]))
+    assert (np.abs(C[:4096, :4096] - C_dev[:4096, :4096]) <= 2 * tol).all()
