@@ -663,12 +663,15 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
         return cudaMemcpy2DAsync(dC + r0 + c0 * dlc, dlc * 8, C + r0 + c0 * ldc, ldc * 8, (r1 - r0) * 8, c1 - c0,
                                  cudaMemcpyHostToDevice, c.s_up);
     };
-    // Block (0, 0) in two k halves when K is deep (4 x 4 pipelines, K >= 8192): the first
-    // call needs only half of op(A) row block 0 and op(B) column block 0, which halves the
-    // exposed upload; the second accumulates onto it (beta = 1) and carries the fault plan, so
-    // reports are those of the one-call block.  ev_up[7] marks the first halves.
-    const bool ksplit = readAB && nrb == 4 && ncb <= 7 && K >= 8192;
-    const long long K1 = ksplit ? (K / 2) / BK * BK : K;
+    // Block (0, 0) in KP k parts when K is deep (4 x 4 pipelines; KP = 2 for K >= 8192, 4 for
+    // K >= 16384): the first call needs only 1/KP of op(A) row block 0 and op(B) column block
+    // 0, which is all of the upload that is exposed; each later part accumulates onto the
+    // previous (beta = 1) and the last carries the fault plan, so reports are those of the
+    // one-call block.  ev_up[ncb + p] marks part p's operands (parts 0 .. KP-2).
+    const int KP = (readAB && nrb == 4 && ncb <= 4) ? (K >= 16384 ? 4 : (K >= 8192 ? 2 : 1)) : 1;
+    const bool ksplit = KP > 1;
+    auto kpart = [&](int p) { return p >= KP ? K : (K * p / KP) / BK * BK; };  // part p = [kpart(p), kpart(p+1))
+    const long long K1 = kpart(KP - 1);  // start of the last part (uploaded with the full blocks)
     auto up_A_k = [&](long long rb, long long k0, long long k1) -> cudaError_t {
         long long r0, r1;
         split(tiles_m, nrb, rb, FTBLAS_TILE_M, M, r0, r1);
@@ -688,10 +691,12 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
                                  cudaMemcpyHostToDevice, c.s_up);
     };
     if (ksplit) {
-        CK(up_A_k(0, 0, K1), "H2D A");
-        CK(up_B_k(0, 0, K1), "H2D B");
-        CK(up_C0(0, 0), "H2D C");
-        CK(cudaEventRecord(c.ev_up[7], c.s_up), "event");
+        for (int p = 0; p + 1 < KP; p++) {
+            CK(up_A_k(0, kpart(p), kpart(p + 1)), "H2D A");
+            CK(up_B_k(0, kpart(p), kpart(p + 1)), "H2D B");
+            if (p == 0) CK(up_C0(0, 0), "H2D C");
+            CK(cudaEventRecord(c.ev_up[ncb + p], c.s_up), "event");
+        }
         CK(up_A_k(0, K1, K), "H2D A");
     } else {
         CK(up_A(0), "H2D A");
@@ -718,16 +723,17 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
         for (long long cb = 0; cb < ncb; cb++) CK(up_C0(rb, cb), "H2D C");
         CK(cudaEventRecord(c.ev_a[rb], c.s_up), "event");
     }
-    if (ksplit) {  // first k half of block (0, 0): no fault injection, report reset
+    for (int p = 0; p + 1 < KP; p++) {  // k parts 0 .. KP-2 of block (0, 0): no fault injection
         long long c0, c1;
         split(tiles_n, ncb, 0, FTBLAS_TILE_N, N, c0, c1);
         long long r0, r1;
         split(tiles_m, nrb, 0, FTBLAS_TILE_M, M, r0, r1);
-        CK(cudaStreamWaitEvent(c.stream, c.ev_up[7], 0), "wait");
-        const double *Ab = is_t(transA) ? dA + r0 * dla : dA + r0;
-        const double *Bb = is_t(transB) ? dB + c0 : dB + c0 * dlb;
-        rc = dgemm_impl(true, transA, transB, r1 - r0, c1 - c0, K1, alpha, Ab, dla, Bb, dlb, beta, dC + r0 + c0 * dlc,
-                        dlc, nullptr, r0, c0, false, false, false);
+        CK(cudaStreamWaitEvent(c.stream, c.ev_up[ncb + p], 0), "wait");
+        const long long k0 = kpart(p);
+        const double *Ak = is_t(transA) ? dA + r0 * dla + k0 : dA + r0 + k0 * dla;
+        const double *Bk = is_t(transB) ? dB + c0 + k0 * dlb : dB + c0 * dlb + k0;
+        rc = dgemm_impl(true, transA, transB, r1 - r0, c1 - c0, kpart(p + 1) - k0, alpha, Ak, dla, Bk, dlb,
+                        p == 0 ? beta : 1.0, dC + r0 + c0 * dlc, dlc, nullptr, r0, c0, p > 0, false, false);
         if (rc) return rc;
     }
     for (long long rb = 0; rb < nrb; rb++) {
@@ -741,7 +747,7 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
             if (rb == 0) CK(cudaStreamWaitEvent(c.stream, c.ev_up[cb], 0), "wait");
             const double *Bb = readAB ? (is_t(transB) ? dB + c0 : dB + c0 * dlb) : nullptr;
             const bool first = rb == 0 && cb == 0;
-            if (first && ksplit) {  // second k half of block (0, 0) onto the first (beta = 1)
+            if (first && ksplit) {  // last k part of block (0, 0) onto the earlier ones (beta = 1)
                 const double *Ak = is_t(transA) ? Ab + K1 : Ab + K1 * dla;
                 const double *Bk = is_t(transB) ? Bb + K1 * dlb : Bb + K1;
                 rc = dgemm_impl(true, transA, transB, r1 - r0, c1 - c0, K - K1, alpha, Ak, dla, Bk, dlb, 1.0,

@@ -441,15 +441,15 @@ def test_host_entry_4x4_blocks_bitwise_equal_device():
     assert np.array_equal(C, C_dev)
 
 
-@pytest.mark.parametrize("tA,tB", [("N", "N"), ("T", "T")])
-def test_host_entry_ksplit_first_block(tA, tB):
-    """The e2e entry at a depth that splits pipeline block (0, 0) into two k halves
-    (16384^2 x 8192, 4 x 4 blocks, beta != 0, 150 flips, both transposes): same report as the
+@pytest.mark.parametrize("tA,tB,K", [("N", "N", 8192), ("T", "T", 8192), ("N", "T", 16384)])
+def test_host_entry_ksplit_first_block(tA, tB, K):
+    """The e2e entry at depths that split pipeline block (0, 0) into k parts (16384^2 x K,
+    4 x 4 blocks: 2 parts at K = 8192, 4 at 16384; beta != 0, 150 flips): same report as the
     single device call, C within the elementwise bound of it (the split block sums in another
     order; every other block is bitwise equal)."""
     import torch
     ft = _lib("gemm")
-    w = syn.Workload("hb5", 16384, 16384, 8192, tA, tB, 1.25, -0.5, "uniform", True, seed=43, n_flips=150)
+    w = syn.Workload("hb5", 16384, 16384, K, tA, tB, 1.25, -0.5, "uniform", True, seed=43, n_flips=150)
     d = syn.make_inputs(w)
     plan = syn.fault_plan(w.M, w.N, w.n_flips, w.seed)
     C_dev, rep_dev = run_gpu(ft, w, d, plan=plan)
@@ -471,3 +471,4 @@ def test_host_entry_ksplit_first_block(tA, tB):
     ab = np.abs(opA[:4096, :]) @ np.abs(opB[:, :4096])
     tol = gemm_bound(w.K, w.alpha, w.beta, ab, np.abs(d["C"][:4096, :4096]))
     assert (np.abs(C[:4096, :4096] - C_dev[:4096, :4096]) <= 2 * tol).all()
+    del C, C_dev, d
