@@ -117,9 +117,14 @@ int ftblas_dgemm_noft(char transA, char transB, int64_t M, int64_t N, int64_t K,
                       double *C, int64_t ldc);
 
 /* ftblas_dgemm on HOST buffers (end-to-end path): copies op(A), op(B) and C
- * (if beta != 0) host->device, runs ftblas_dgemm, copies C device->host and
- * synchronizes.  err_report as above (may be NULL).  Pinned host memory gives
- * the full PCIe bandwidth; pageable memory works but is slower. */
+ * (if beta != 0) host->device, runs the ABFT DGEMM, copies C device->host and
+ * synchronizes.  Pipelined over blocks of whole 128 x 128 tiles (uploads, block
+ * GEMMs and downloads on three streams); for deep K the first block runs in k
+ * parts accumulated with beta = 1 (the fault plan applies to the last part, so
+ * the report equals the one-call report; the split block's C can differ from
+ * ftblas_dgemm's in rounding order, within the usual bound).  err_report as
+ * above (may be NULL).  Pinned host memory gives the full PCIe bandwidth;
+ * pageable memory works but is slower. */
 int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K, double alpha,
                       const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
                       double *C, int64_t ldc, ftblas_err_report *err_report);
