@@ -51,7 +51,7 @@ struct Ctx {
     DevBuf hA, hB, hC;    // ftblas_dgemm_host device staging
     cudaStream_t s_up = nullptr, s_down = nullptr;  // ftblas_dgemm_host copy streams
     cudaStream_t s_side = nullptr;                   // checksum GEMM S^T (forked / joined)
-    cudaEvent_t ev_entry = nullptr, ev_exit = nullptr, ev_up[8] = {}, ev_done[16] = {}, ev_a[4] = {};
+    cudaEvent_t ev_entry = nullptr, ev_exit = nullptr, ev_up[8] = {}, ev_done[16] = {}, ev_a[4] = {}, ev_kp[16] = {};
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // cached A-side encoding (FTBLAS_REUSE_A_ENCODE)
     struct AKey {
@@ -76,6 +76,7 @@ struct Ctx {
         for (int q = 0; q < 8 && e == cudaSuccess; q++) e = cudaEventCreateWithFlags(&ev_up[q], cudaEventDisableTiming);
         for (int q = 0; q < 16 && e == cudaSuccess; q++) e = cudaEventCreateWithFlags(&ev_done[q], cudaEventDisableTiming);
         for (int q = 0; q < 4 && e == cudaSuccess; q++) e = cudaEventCreateWithFlags(&ev_a[q], cudaEventDisableTiming);
+        for (int q = 0; q < 16 && e == cudaSuccess; q++) e = cudaEventCreateWithFlags(&ev_kp[q], cudaEventDisableTiming);
         return e;
     }
     long long launches = 0;
@@ -663,11 +664,13 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
         return cudaMemcpy2DAsync(dC + r0 + c0 * dlc, dlc * 8, C + r0 + c0 * ldc, ldc * 8, (r1 - r0) * 8, c1 - c0,
                                  cudaMemcpyHostToDevice, c.s_up);
     };
-    // Block (0, 0) in KP k parts when K is deep (4 x 4 pipelines; KP = 2 for K >= 8192, 4 for
-    // K >= 16384): the first call needs only 1/KP of op(A) row block 0 and op(B) column block
-    // 0, which is all of the upload that is exposed; each later part accumulates onto the
-    // previous (beta = 1) and the last carries the fault plan, so reports are those of the
-    // one-call block.  ev_up[ncb + p] marks part p's operands (parts 0 .. KP-2).
+    // Row block 0 in KP k parts when K is deep (4 x 4 pipelines; KP = 2 for K >= 8192, 4 for
+    // K >= 16384): uploads go in k order (op(A) row block 0 part p, then part p of every op(B)
+    // column block), so the first call needs only 1/KP of op(A) block 0 and op(B) block 0 --
+    // all of the upload that is exposed -- and every later call finds its operands already
+    // up.  Each later part accumulates onto the previous (beta = 1); the last part carries the
+    // fault plan, so reports are those of one call per block.  ev_kp[4 cb + p] marks part p of
+    // column block cb (parts 0 .. KP-2); the last parts complete with ev_a[0] / ev_up[cb].
     const int KP = (readAB && nrb == 4 && ncb <= 4) ? (K >= 16384 ? 4 : (K >= 8192 ? 2 : 1)) : 1;
     const bool ksplit = KP > 1;
     auto kpart = [&](int p) { return p >= KP ? K : (K * p / KP) / BK * BK; };  // part p = [kpart(p), kpart(p+1))
@@ -693,9 +696,11 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
     if (ksplit) {
         for (int p = 0; p + 1 < KP; p++) {
             CK(up_A_k(0, kpart(p), kpart(p + 1)), "H2D A");
-            CK(up_B_k(0, kpart(p), kpart(p + 1)), "H2D B");
-            if (p == 0) CK(up_C0(0, 0), "H2D C");
-            CK(cudaEventRecord(c.ev_up[ncb + p], c.s_up), "event");
+            for (long long cb = 0; cb < ncb; cb++) {
+                CK(up_B_k(cb, kpart(p), kpart(p + 1)), "H2D B");
+                if (p == 0) CK(up_C0(0, cb), "H2D C");
+                CK(cudaEventRecord(c.ev_kp[4 * cb + p], c.s_up), "event");
+            }
         }
         CK(up_A_k(0, K1, K), "H2D A");
     } else {
@@ -705,8 +710,8 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
     for (long long cb = 0; cb < ncb; cb++) {
         long long c0, c1;
         split(tiles_n, ncb, cb, FTBLAS_TILE_N, N, c0, c1);
-        if (ksplit && cb == 0) {
-            CK(up_B_k(0, K1, K), "H2D B");
+        if (ksplit) {
+            CK(up_B_k(cb, K1, K), "H2D B");
         } else if (readAB) {
             if (is_t(transB))  // op(B)(:, c0:c1) = rows c0..c1 of the N x K stored B
                 CK(cudaMemcpy2DAsync(dB + c0, dlb * 8, B + c0, ldb * 8, (c1 - c0) * 8, K, cudaMemcpyHostToDevice,
@@ -715,7 +720,7 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
                 CK(cudaMemcpy2DAsync(dB + c0 * dlb, dlb * 8, B + c0 * ldb, ldb * 8, K * 8, c1 - c0,
                                      cudaMemcpyHostToDevice, c.s_up), "H2D B");
         }
-        if (!(ksplit && cb == 0)) CK(up_C0(0, cb), "H2D C");
+        if (!ksplit) CK(up_C0(0, cb), "H2D C");
         CK(cudaEventRecord(c.ev_up[cb], c.s_up), "event");
     }
     for (long long rb = 1; rb < nrb; rb++) {
@@ -723,18 +728,21 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
         for (long long cb = 0; cb < ncb; cb++) CK(up_C0(rb, cb), "H2D C");
         CK(cudaEventRecord(c.ev_a[rb], c.s_up), "event");
     }
-    for (int p = 0; p + 1 < KP; p++) {  // k parts 0 .. KP-2 of block (0, 0): no fault injection
-        long long c0, c1;
-        split(tiles_n, ncb, 0, FTBLAS_TILE_N, N, c0, c1);
+    for (int p = 0; p + 1 < KP; p++) {  // k parts 0 .. KP-2 of row block 0: no fault injection
         long long r0, r1;
         split(tiles_m, nrb, 0, FTBLAS_TILE_M, M, r0, r1);
-        CK(cudaStreamWaitEvent(c.stream, c.ev_up[ncb + p], 0), "wait");
-        const long long k0 = kpart(p);
-        const double *Ak = is_t(transA) ? dA + r0 * dla + k0 : dA + r0 + k0 * dla;
-        const double *Bk = is_t(transB) ? dB + c0 + k0 * dlb : dB + c0 * dlb + k0;
-        rc = dgemm_impl(true, transA, transB, r1 - r0, c1 - c0, kpart(p + 1) - k0, alpha, Ak, dla, Bk, dlb,
-                        p == 0 ? beta : 1.0, dC + r0 + c0 * dlc, dlc, nullptr, r0, c0, p > 0, false, false);
-        if (rc) return rc;
+        for (long long cb = 0; cb < ncb; cb++) {
+            long long c0, c1;
+            split(tiles_n, ncb, cb, FTBLAS_TILE_N, N, c0, c1);
+            CK(cudaStreamWaitEvent(c.stream, c.ev_kp[4 * cb + p], 0), "wait");
+            const long long k0 = kpart(p);
+            const double *Ak = is_t(transA) ? dA + r0 * dla + k0 : dA + r0 + k0 * dla;
+            const double *Bk = is_t(transB) ? dB + c0 + k0 * dlb : dB + c0 * dlb + k0;
+            rc = dgemm_impl(true, transA, transB, r1 - r0, c1 - c0, kpart(p + 1) - k0, alpha, Ak, dla, Bk, dlb,
+                            p == 0 ? beta : 1.0, dC + r0 + c0 * dlc, dlc, nullptr, r0, c0, p > 0 || cb > 0, false,
+                            false);
+            if (rc) return rc;
+        }
     }
     for (long long rb = 0; rb < nrb; rb++) {
         long long r0, r1;
@@ -747,7 +755,7 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
             if (rb == 0) CK(cudaStreamWaitEvent(c.stream, c.ev_up[cb], 0), "wait");
             const double *Bb = readAB ? (is_t(transB) ? dB + c0 : dB + c0 * dlb) : nullptr;
             const bool first = rb == 0 && cb == 0;
-            if (first && ksplit) {  // last k part of block (0, 0) onto the earlier ones (beta = 1)
+            if (rb == 0 && ksplit) {  // last k part of a row-0 block onto the earlier ones (beta = 1)
                 const double *Ak = is_t(transA) ? Ab + K1 : Ab + K1 * dla;
                 const double *Bk = is_t(transB) ? Bb + K1 * dlb : Bb + K1;
                 rc = dgemm_impl(true, transA, transB, r1 - r0, c1 - c0, K - K1, alpha, Ak, dla, Bk, dlb, 1.0,
