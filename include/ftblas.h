@@ -119,9 +119,9 @@ int ftblas_dgemm_noft(char transA, char transB, int64_t M, int64_t N, int64_t K,
 /* ftblas_dgemm on HOST buffers (end-to-end path): copies op(A), op(B) and C
  * (if beta != 0) host->device, runs the ABFT DGEMM, copies C device->host and
  * synchronizes.  Pipelined over blocks of whole 128 x 128 tiles (uploads, block
- * GEMMs and downloads on three streams); for deep K the first block runs in k
- * parts accumulated with beta = 1 (the fault plan applies to the last part, so
- * the report equals the one-call report; the split block's C can differ from
+ * GEMMs and downloads on three streams); for deep K the first row block runs in
+ * k parts accumulated with beta = 1 (the fault plan applies to the last parts, so
+ * the report equals the one-call report; those blocks' C can differ from
  * ftblas_dgemm's in rounding order, within the usual bound).  err_report as
  * above (may be NULL).  Pinned host memory gives the full PCIe bandwidth;
  * pageable memory works but is slower. */
