@@ -275,7 +275,10 @@ def main():
 
     # N > 1: op(B) is broadcast in column chunks of whole tiles, the GEMM of chunk c overlapping
     # the broadcast of chunks > c (shard.sharded_dgemm); N = 1: one call, no exchange.
-    chunks = shard.broadcast_chunk_bounds(m, w.N) if (world > 1 and w.transB == "N") else 1
+    # the chunk bounds must be identical on every rank (each chunk is one collective):
+    # computed from rank 0's row count, the largest shard
+    m_ref = shard.shard_rows(w.M, world, 0)[1] - shard.shard_rows(w.M, world, 0)[0]
+    chunks = shard.broadcast_chunk_bounds(m_ref, w.N) if (world > 1 and w.transB == "N") else 1
 
     def step(gemm, broadcast):
         # C := alpha AB + beta C accumulates into C; the value drifts but the work is identical

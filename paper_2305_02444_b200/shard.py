@@ -102,7 +102,8 @@ def sharded_dgemm(gemm, transA, transB, M, N, K, alpha, A_shard, lda, B, ldb, be
     column-major storage of B (ld ``ldb``).
 
     The exchange of the step is the broadcast of op(B) from ``src``.  With ``chunks`` > 1 (a
-    count, or an explicit list of column blocks such as ``broadcast_chunk_bounds``) and
+    count, or an explicit list of column blocks such as ``broadcast_chunk_bounds`` -- the same
+    list on every rank, since each block is one collective) and
     transB = 'N' (column blocks of op(B) are contiguous in B) it is split into column blocks
     of whole tiles, all posted asynchronously on the communication stream; the GEMM of block
     c waits only for block c, so the broadcast of the later blocks overlaps the DMMA work of

@@ -61,6 +61,10 @@ def _worker(rank, world, port, tA, chunks, q):
                 e["tile_n"] = int(e["tile_n"]) + col_offset // 128
                 captured["entries"].append(e)
 
+        if chunks == "geo":  # explicit geometric bounds, from rank 0's (largest) shard on every rank
+            m_ref = shard.shard_rows(w.M, world, 0)[1] - shard.shard_rows(w.M, world, 0)[0]
+            chunks = shard.broadcast_chunk_bounds(m_ref, w.N, sms=2)
+            assert len(chunks) == 2
         shard.sharded_dgemm(cpu_gemm, tA, "N", w.M, w.N, w.K, w.alpha, A_loc, lda, B_t, d["ldb"],
                             w.beta, C_flat, max(1, m), rank=rank, world=world, chunks=chunks)
         C_loc = C_flat.numpy().reshape((max(1, m), w.N), order="F")[:m]
@@ -73,7 +77,7 @@ def _worker(rank, world, port, tA, chunks, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("tA,chunks", [("N", 1), ("T", 1), ("N", 2), ("T", 3)])
+@pytest.mark.parametrize("tA,chunks", [("N", 1), ("T", 1), ("N", 2), ("T", 3), ("N", "geo")])
 def test_sharded_equals_unsharded(tA, chunks):
     world = 2
     ctx = mp.get_context("spawn")
