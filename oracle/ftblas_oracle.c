@@ -145,9 +145,27 @@ void ora_encode_b(int tB, i64 K, const double *B, i64 ldb, i64 j0, i64 j1,
  * with beta*C0 encoded alongside (line 558):
  *   crow[i] = alpha * sum_k op(A)(i,k) br[k]  + beta * sum_{j in J} C0(i,j)     (C e)
  *   ccol[j] = alpha * sum_k ac[k] op(B)(k,j)  + beta * sum_{i in I} C0(i,j)     (e^T C)
- * and the absolute C0 sums used by the threshold (reading R4):
- *   c0row[i] = sum_{j in J} |C0(i,j)|,  c0col[j] = sum_{i in I} |C0(i,j)|.
+ * and the bounds of the absolute C0 sums used by the threshold (readings R4, R4k):
+ *   c0row[i] = |J| * up(max_{j in J} |C0(i,j)|)  >=  sum_{j in J} |C0(i,j)|,
+ *   c0col[j] = |I| * up(max_{i in I} |C0(i,j)|)  >=  sum_{i in I} |C0(i,j)|,
+ * up(x) = the binary64 whose high 32-bit word is that of x plus one and whose low word is
+ * zero (the smallest such double above x; +Inf when x is Inf/NaN or in the top binade step).
  * beta == 0: C0 is not read and the C0 terms are 0. */
+/* High 32-bit word of |x| (sign cleared): integer maxima of it order non-negative doubles. */
+static uint32_t abs_hi(double x) {
+    uint64_t b;
+    memcpy(&b, &x, 8);
+    return (uint32_t)(b >> 32) & 0x7fffffffu;
+}
+/* n * up(m) for the maximum high word h of |C0| over n elements (reading R4k). */
+double ora_c0_bound(i64 n, uint32_t h) {
+    if (h >= 0x7ff00000u) return INFINITY;
+    uint64_t b = (uint64_t)(h + 1u) << 32;
+    double up;
+    memcpy(&up, &b, 8);
+    return (double)n * up;
+}
+
 void ora_ref_checksums(int tA, int tB, i64 K, double alpha, const double *A, i64 lda,
                        const double *B, i64 ldb, double beta, const double *C0, i64 ldc,
                        i64 i0, i64 i1, i64 j0, i64 j1, const double *ac, const double *br,
@@ -155,26 +173,28 @@ void ora_ref_checksums(int tA, int tB, i64 K, double alpha, const double *A, i64
     for (i64 i = i0; i < i1; i++) {
         double r = 0.0;
         for (i64 k = 0; k < K; k++) r += opA(A, lda, tA, i, k) * br[k];
-        double c = 0.0, ca = 0.0;
+        double c = 0.0;
+        uint32_t h = 0;
         if (beta != 0.0)
             for (i64 j = j0; j < j1; j++) {
                 c += C0[i + j * ldc];
-                ca += fabs(C0[i + j * ldc]);
+                if (abs_hi(C0[i + j * ldc]) > h) h = abs_hi(C0[i + j * ldc]);
             }
         crow[i - i0] = beta == 0.0 ? alpha * r : alpha * r + beta * c;
-        c0row[i - i0] = ca;
+        c0row[i - i0] = beta == 0.0 ? 0.0 : ora_c0_bound(j1 - j0, h);
     }
     for (i64 j = j0; j < j1; j++) {
         double s = 0.0;
         for (i64 k = 0; k < K; k++) s += ac[k] * opB(B, ldb, tB, k, j);
-        double c = 0.0, ca = 0.0;
+        double c = 0.0;
+        uint32_t h = 0;
         if (beta != 0.0)
             for (i64 i = i0; i < i1; i++) {
                 c += C0[i + j * ldc];
-                ca += fabs(C0[i + j * ldc]);
+                if (abs_hi(C0[i + j * ldc]) > h) h = abs_hi(C0[i + j * ldc]);
             }
         ccol[j - j0] = beta == 0.0 ? alpha * s : alpha * s + beta * c;
-        c0col[j - j0] = ca;
+        c0col[j - j0] = beta == 0.0 ? 0.0 : ora_c0_bound(i1 - i0, h);
     }
 }
 
@@ -194,9 +214,10 @@ typedef struct {
     i64 cols_flagged;  /* total flagged columns */
 } ora_stats;
 
-/* Threshold (reading R4):  tau = 4 u (K + n + 3) * rho,  rho an upper bound of the
- * absolute checksum |alpha| (|A||B| e)_i + |beta| (|C0| e)_i built from norms.  The flag
- * test is written !(x <= tau) so that NaN/Inf residuals are flagged. */
+/* Threshold (readings R4, R4k):  tau = 4 u (K + n + 3) * rho,  rho an upper bound of the
+ * absolute checksum |alpha| (|A||B| e)_i + |beta| (|C0| e)_i built from norms and the
+ * rounded-up |C0| maxima (c0row / c0col above).  The flag test is written !(x <= tau) so
+ * that NaN/Inf residuals are flagged. */
 static int flagged(double resid, double tau) { return !(fabs(resid) <= tau); }
 
 /* Verify one tile, locate and correct (lines 517, 540, 521; readings R5-R7).

@@ -42,17 +42,22 @@ struct Ctx {
     DevBuf ws;            // encode outputs
     DevBuf rep;           // ReportHdr + entries
     long long rep_cap = 1 << 16;
-    DevBuf plan_dev;      // fault plan arrays
-    DevBuf plan_ptr_dev;  // CSR offsets for the last (M,N) shape
-    long long plan_ptr_M = -1, plan_ptr_N = -1, plan_version = 0, plan_uploaded = -1, plan_off_i = 0, plan_off_j = 0;
-    long long plan_n_dev = 0;
+    DevBuf plan_dev;      // fault plan: i, j (caller coordinates), bit, CSR offsets by caller tile
+    long long plan_version = 0, plan_uploaded = -1;
+    void *plan_host = nullptr;  // pinned staging of the plan upload
+    size_t plan_host_bytes = 0;
+    cudaEvent_t ev_plan = nullptr;
     std::vector<long long> plan_i, plan_j;
     std::vector<int> plan_bit;
     DevBuf hA, hB, hC;    // ftblas_dgemm_host device staging
     cudaStream_t s_up = nullptr, s_down = nullptr;  // ftblas_dgemm_host copy streams
     cudaStream_t s_side = nullptr;                   // checksum GEMM S^T (forked / joined)
-    cudaEvent_t ev_entry = nullptr, ev_exit = nullptr, ev_up[8] = {}, ev_done[16] = {}, ev_a[4] = {}, ev_kp[16] = {};
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // ftblas_dgemm_host pipeline events: at most HOST_MAX_RB row blocks x HOST_MAX_CB column
+    // blocks and HOST_MAX_KP k parts (checked against the block policy before any use)
+    static constexpr int HOST_MAX_RB = 4, HOST_MAX_CB = 8, HOST_MAX_BLOCKS = 16, HOST_MAX_KP = 4;
+    cudaEvent_t ev_entry = nullptr, ev_exit = nullptr, ev_up[HOST_MAX_CB] = {}, ev_done[HOST_MAX_BLOCKS] = {},
+                ev_a[HOST_MAX_RB] = {}, ev_kp[HOST_MAX_CB * HOST_MAX_KP] = {};
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_switch = nullptr;
     // cached A-side encoding (FTBLAS_REUSE_A_ENCODE)
     struct AKey {
         const void *A; long long lda, M, K; bool kc, a0;
@@ -71,12 +76,13 @@ struct Ctx {
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s_side, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_switch, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_entry, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_exit, cudaEventDisableTiming);
-        for (int q = 0; q < 8 && e == cudaSuccess; q++) e = cudaEventCreateWithFlags(&ev_up[q], cudaEventDisableTiming);
-        for (int q = 0; q < 16 && e == cudaSuccess; q++) e = cudaEventCreateWithFlags(&ev_done[q], cudaEventDisableTiming);
-        for (int q = 0; q < 4 && e == cudaSuccess; q++) e = cudaEventCreateWithFlags(&ev_a[q], cudaEventDisableTiming);
-        for (int q = 0; q < 16 && e == cudaSuccess; q++) e = cudaEventCreateWithFlags(&ev_kp[q], cudaEventDisableTiming);
+        for (cudaEvent_t &x : ev_up) if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+        for (cudaEvent_t &x : ev_done) if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+        for (cudaEvent_t &x : ev_a) if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+        for (cudaEvent_t &x : ev_kp) if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
         return e;
     }
     long long launches = 0;
@@ -217,57 +223,59 @@ bool vec_ok(const void *p, long long ld) {
     return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && (ld % 2 == 0);
 }
 
-// Upload the CSR (by tile, tile index tn*ntm + tm) of the fault plan restricted to the call's
-// block [off_i, off_i + M) x [off_j, off_j + N) of the caller's C, in call-relative indices.
-int prepare_plan(long long M, long long N, long long off_i, long long off_j, GemmArgs &g) {
+// Upload the fault plan once per plan version, in the caller's coordinates: CSR by the
+// caller's 128 x 128 tile (index gtn * plan_ntm + gtm over the grid that covers every planned
+// element).  A call on the block at (off_i, off_j) looks its tiles up at (tm + off_i / 128,
+// tn + off_j / 128), so blocked / chunked callers share one upload.  The copy is stream-ordered
+// from a pinned staging buffer (no host stall); the staging buffer is rewritten only after the
+// previous upload has completed (ev_plan).
+int prepare_plan(GemmArgs &g) {
     Ctx &c = ctx();
     g.plan_ptr = nullptr; g.plan_i = nullptr; g.plan_j = nullptr; g.plan_bit = nullptr;
+    g.plan_ntm = 0; g.plan_ntn = 0;
     if (c.plan_i.empty()) return 0;
-    const size_t bytes_ij0 = std::max<size_t>(1, c.plan_i.size()) * sizeof(long long);
-    if (c.plan_uploaded == c.plan_version && c.plan_ptr_M == M && c.plan_ptr_N == N && c.plan_off_i == off_i &&
-        c.plan_off_j == off_j) {  // cached upload
-        char *base = c.plan_dev.as<char>();
-        g.plan_ptr = c.plan_ptr_dev.as<int>();
-        g.plan_i = reinterpret_cast<const long long *>(base);
-        g.plan_j = reinterpret_cast<const long long *>(base + bytes_ij0);
-        g.plan_bit = reinterpret_cast<const int *>(base + 2 * bytes_ij0);
-        return 0;
+    const size_t n = c.plan_i.size();
+    const size_t bytes_ij = n * sizeof(long long), bytes_b = (n * sizeof(int) + 15) / 16 * 16;
+    long long ntm = 1, ntn = 1;
+    for (size_t f = 0; f < n; f++) {
+        ntm = std::max(ntm, c.plan_i[f] / BM + 1);
+        ntn = std::max(ntn, c.plan_j[f] / BN + 1);
     }
-    const long long ntm = (M + BM - 1) / BM, ntn = (N + BN - 1) / BN, nt = ntm * ntn;
-    std::vector<int> cnt(nt + 1, 0);
-    std::vector<long long> order;
-    for (size_t f = 0; f < c.plan_i.size(); f++) {
-        const long long i = c.plan_i[f] - off_i, j = c.plan_j[f] - off_j;
-        if (i < 0 || i >= M || j < 0 || j >= N) continue;
-        cnt[(j / BN) * ntm + i / BM + 1]++;
-        order.push_back((long long)f);
+    const long long nt = ntm * ntn;
+    const size_t bytes_ptr = (size_t)(nt + 1) * sizeof(int);
+    const size_t total = 2 * bytes_ij + bytes_b + bytes_ptr;
+    if (c.plan_uploaded != c.plan_version) {
+        std::vector<int> cnt(nt + 1, 0);
+        for (size_t f = 0; f < n; f++) cnt[(c.plan_j[f] / BN) * ntm + c.plan_i[f] / BM + 1]++;
+        for (long long t = 0; t < nt; t++) cnt[t + 1] += cnt[t];
+        if (c.ev_plan) CK(cudaEventSynchronize(c.ev_plan), "plan staging reuse");
+        else CK(cudaEventCreateWithFlags(&c.ev_plan, cudaEventDisableTiming), "event");
+        if (c.plan_host_bytes < total) {
+            if (c.plan_host) cudaFreeHost(c.plan_host);
+            c.plan_host = nullptr; c.plan_host_bytes = 0;
+            CK(cudaHostAlloc(&c.plan_host, total, cudaHostAllocDefault), "cudaHostAlloc(plan)");
+            c.plan_host_bytes = total;
+        }
+        char *h = static_cast<char *>(c.plan_host);
+        long long *pi = reinterpret_cast<long long *>(h), *pj = reinterpret_cast<long long *>(h + bytes_ij);
+        int *pb = reinterpret_cast<int *>(h + 2 * bytes_ij);
+        std::memcpy(h + 2 * bytes_ij + bytes_b, cnt.data(), bytes_ptr);
+        std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+        for (size_t f = 0; f < n; f++) {
+            const int pos = fill[(c.plan_j[f] / BN) * ntm + c.plan_i[f] / BM]++;
+            pi[pos] = c.plan_i[f]; pj[pos] = c.plan_j[f]; pb[pos] = c.plan_bit[f];
+        }
+        CK(c.plan_dev.ensure(total), "cudaMalloc(plan)");
+        CK(cudaMemcpyAsync(c.plan_dev.p, h, total, cudaMemcpyHostToDevice, c.stream), "plan upload");
+        CK(cudaEventRecord(c.ev_plan, c.stream), "event");
+        c.plan_uploaded = c.plan_version;
     }
-    for (long long t = 0; t < nt; t++) cnt[t + 1] += cnt[t];
-    std::vector<int> fill(cnt.begin(), cnt.end() - 1);
-    const size_t n = order.size();
-    std::vector<long long> pi(n), pj(n);
-    std::vector<int> pb(n);
-    for (long long f : order) {
-        const long long i = c.plan_i[f] - off_i, j = c.plan_j[f] - off_j;
-        const int pos = fill[(j / BN) * ntm + i / BM]++;
-        pi[pos] = i; pj[pos] = j; pb[pos] = c.plan_bit[f];
-    }
-    const size_t bytes_ij = bytes_ij0;  // sized by the full plan so the cached layout is stable
-    const size_t bytes_b = std::max<size_t>(1, c.plan_i.size()) * sizeof(int);
-    CK(c.plan_dev.ensure(2 * bytes_ij + bytes_b), "cudaMalloc(plan)");
-    CK(c.plan_ptr_dev.ensure((nt + 1) * sizeof(int)), "cudaMalloc(plan_ptr)");
     char *base = c.plan_dev.as<char>();
-    // synchronous copies: the plan is host-side test-harness state, uploaded before the launch
-    CK(cudaMemcpyAsync(base, pi.data(), n * sizeof(long long), cudaMemcpyHostToDevice, c.stream), "plan i");
-    CK(cudaMemcpyAsync(base + bytes_ij, pj.data(), n * sizeof(long long), cudaMemcpyHostToDevice, c.stream), "plan j");
-    CK(cudaMemcpyAsync(base + 2 * bytes_ij, pb.data(), n * sizeof(int), cudaMemcpyHostToDevice, c.stream), "plan bit");
-    CK(cudaMemcpyAsync(c.plan_ptr_dev.p, cnt.data(), (nt + 1) * sizeof(int), cudaMemcpyHostToDevice, c.stream), "plan ptr");
-    CK(cudaStreamSynchronize(c.stream), "plan upload");
-    c.plan_uploaded = c.plan_version; c.plan_ptr_M = M; c.plan_ptr_N = N; c.plan_off_i = off_i; c.plan_off_j = off_j;
-    g.plan_ptr = c.plan_ptr_dev.as<int>();
     g.plan_i = reinterpret_cast<const long long *>(base);
     g.plan_j = reinterpret_cast<const long long *>(base + bytes_ij);
     g.plan_bit = reinterpret_cast<const int *>(base + 2 * bytes_ij);
+    g.plan_ptr = reinterpret_cast<const int *>(base + 2 * bytes_ij + bytes_b);
+    g.plan_ntm = ntm; g.plan_ntn = ntn;
     return 0;
 }
 
@@ -424,9 +432,7 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
         // on the same A (the blocks of a chunked call); its encoding is reused when the cached
         // key matches and the workspace was not reallocated, else A is encoded as usual.
         const Ctx::AKey akey{A, lda, M, K, kca, alpha == 0.0};
-        const bool skip_a = reuse_a && c.a_valid && c.a_key == akey && c.a_ws_gen == c.ws_gen;
-        if (skip_a) kch = c.a_kch;
-        const long long kper = ((Kp + kch - 1) / kch + 31) / 32 * 32;
+        bool skip_a = reuse_a && c.a_valid && c.a_key == akey && c.a_ws_gen == c.ws_gen;
         const bool pre = c.checksum_mode == FTBLAS_CHECKSUM_GEMM;
         long long spR = 1, kpR = Kp, spS = 1, kpS = Kp;
         if (pre) {
@@ -437,12 +443,24 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
         // reuse them), then the B side, then the checksum-GEMM partials
         // (every sub-array starts on a 128-byte boundary: bulk copies and TMA need >= 16 B)
         auto al = [](size_t n) { return (n + 15) / 16 * 16; };
-        const size_t oLA = al((size_t)ntm * Kp), oTA = oLA + al((size_t)kch * M), oWB = oTA + al((size_t)kch * ntm);
-        const size_t oLB = oWB + al((size_t)ntn * Kp), oTB = oLB + al((size_t)kch * N), oR = oTB + al((size_t)kch * ntn);
-        const size_t oS = oR + (pre ? al((size_t)spR * ntn * M) : 0);
-        const size_t oF = oS + (pre ? al((size_t)spS * ntm * N) : 0);  // finalized side data
-        const size_t nF = pre ? (size_t)(M + N + ntm + ntn) + (size_t)ntn * M + (size_t)ntm * N : 0;
-        const size_t need = (oF + nF) * sizeof(double);
+        size_t oLA, oTA, oWB, oLB, oTB, oR, oS, oF, nF, need;
+        auto layout = [&](int kc) {
+            oLA = al((size_t)ntm * Kp); oTA = oLA + al((size_t)kc * M); oWB = oTA + al((size_t)kc * ntm);
+            oLB = oWB + al((size_t)ntn * Kp); oTB = oLB + al((size_t)kc * N); oR = oTB + al((size_t)kc * ntn);
+            oS = oR + (pre ? al((size_t)spR * ntn * M) : 0);
+            oF = oS + (pre ? al((size_t)spS * ntm * N) : 0);  // finalized side data
+            nF = pre ? (size_t)(M + N + ntm + ntn) + (size_t)ntn * M + (size_t)ntm * N : 0;
+            need = (oF + nF) * sizeof(double);
+        };
+        layout(skip_a ? c.a_kch : kch);
+        if (skip_a && need > c.ws.bytes) {
+            // the workspace grows (free + malloc): the cached A encoding does not survive it,
+            // so A is encoded again with this call's own chunk count
+            skip_a = false;
+            layout(kch);
+        }
+        if (skip_a) kch = c.a_kch;
+        const long long kper = ((Kp + kch - 1) / kch + 31) / 32 * 32;
         const size_t nRS = pre ? (size_t)spR * ntn * M + (size_t)spS * ntm * N : 0;
         if (need > c.ws.bytes) c.ws_gen++;
         CK(c.ws.ensure(need), "cudaMalloc(workspace)");
@@ -469,9 +487,10 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
         g.rep_cap = c.rep_cap;
         g.vecC = vec_ok(C, ldc) ? 1 : 0;
         g.off_i = off_i; g.off_j = off_j;
-        rc = prepare_plan(M, N, off_i, off_j, g);
-        if (rc) return rc;
-        if (!inject) { g.plan_ptr = nullptr; g.plan_i = nullptr; g.plan_j = nullptr; g.plan_bit = nullptr; }
+        if (inject) {
+            rc = prepare_plan(g);
+            if (rc) return rc;
+        }
         EncodeArgs ea{};
         const EncodeOperand opA{A, lda, M, kca ? 1 : 0, va ? 1 : 0, const_cast<double *>(g.VA), lineA, tmaxA, (int)ntm};
         const EncodeOperand opB{B, ldb, N, kcb ? 1 : 0, vb ? 1 : 0, const_cast<double *>(g.WB), lineB, tmaxB, (int)ntn};
@@ -672,6 +691,10 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
     // fault plan, so reports are those of one call per block.  ev_kp[4 cb + p] marks part p of
     // column block cb (parts 0 .. KP-2); the last parts complete with ev_a[0] / ev_up[cb].
     const int KP = (readAB && nrb == 4 && ncb <= 4) ? (K >= 16384 ? 4 : (K >= 8192 ? 2 : 1)) : 1;
+    static_assert(Ctx::HOST_MAX_RB * 4 <= Ctx::HOST_MAX_BLOCKS && Ctx::HOST_MAX_CB * 2 <= Ctx::HOST_MAX_BLOCKS,
+                  "block policies (4 x 4, 2 x 8, 1 x 8) must fit the event arrays");
+    if (nrb > Ctx::HOST_MAX_RB || ncb > Ctx::HOST_MAX_CB || nrb * ncb > Ctx::HOST_MAX_BLOCKS || KP > Ctx::HOST_MAX_KP)
+        return cuda_fail(cudaErrorInvalidConfiguration, "ftblas_dgemm_host: block policy exceeds the event arrays");
     const bool ksplit = KP > 1;
     auto kpart = [&](int p) { return p >= KP ? K : (K * p / KP) / BK * BK; };  // part p = [kpart(p), kpart(p+1))
     const long long K1 = kpart(KP - 1);  // start of the last part (uploaded with the full blocks)
@@ -699,7 +722,7 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
             for (long long cb = 0; cb < ncb; cb++) {
                 CK(up_B_k(cb, kpart(p), kpart(p + 1)), "H2D B");
                 if (p == 0) CK(up_C0(0, cb), "H2D C");
-                CK(cudaEventRecord(c.ev_kp[4 * cb + p], c.s_up), "event");
+                CK(cudaEventRecord(c.ev_kp[Ctx::HOST_MAX_KP * cb + p], c.s_up), "event");
             }
         }
         CK(up_A_k(0, K1, K), "H2D A");
@@ -734,7 +757,7 @@ int ftblas_dgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
         for (long long cb = 0; cb < ncb; cb++) {
             long long c0, c1;
             split(tiles_n, ncb, cb, FTBLAS_TILE_N, N, c0, c1);
-            CK(cudaStreamWaitEvent(c.stream, c.ev_kp[4 * cb + p], 0), "wait");
+            CK(cudaStreamWaitEvent(c.stream, c.ev_kp[Ctx::HOST_MAX_KP * cb + p], 0), "wait");
             const long long k0 = kpart(p);
             const double *Ak = is_t(transA) ? dA + r0 * dla + k0 : dA + r0 + k0 * dla;
             const double *Bk = is_t(transB) ? dB + c0 + k0 * dlb : dB + c0 * dlb + k0;
@@ -816,7 +839,15 @@ int ftblas_set_tile_policy(int policy) {
 int ftblas_get_tile_policy(void) { return ctx().tile_policy; }
 
 int ftblas_set_stream(void *stream) {
-    ctx().stream = static_cast<cudaStream_t>(stream);
+    Ctx &c = ctx();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (s == c.stream) return 0;
+    // the workspace, report and fault-plan buffers are shared by all calls: work enqueued on
+    // the new stream is ordered after everything already enqueued on the old one
+    CK(c.ensure_copy_streams(), "streams");
+    CK(cudaEventRecord(c.ev_switch, c.stream), "event");
+    CK(cudaStreamWaitEvent(s, c.ev_switch, 0), "wait");
+    c.stream = s;
     return 0;
 }
 
@@ -856,7 +887,7 @@ const char *ftblas_last_error(void) { return ctx().err; }
 int ftblas_release(void) {
     Ctx &c = ctx();
     cudaStreamSynchronize(c.stream);
-    c.ws.release(); c.ws_gen++; c.a_valid = false; c.rep.release(); c.plan_dev.release(); c.plan_ptr_dev.release();
+    c.ws.release(); c.ws_gen++; c.a_valid = false; c.rep.release(); c.plan_dev.release();
     c.plan_uploaded = -1;
     c.hA.release(); c.hB.release(); c.hC.release();
     return 0;

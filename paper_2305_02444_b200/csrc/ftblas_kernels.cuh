@@ -141,10 +141,12 @@ struct GemmArgs {
     const double *fin_nrmA, *fin_nrmB;  // M, N  : ||op(A)(i,:)||_1, ||op(B)(:,j)||_1
     const double *fin_maxA, *fin_maxB;  // ntm, ntn: tile maxima of the column / row |.| sums
     const double *fin_R, *fin_S;        // FT_PRE: ntn x M, ntm x N (checksum GEMM results)
-    // fault plan (CSR by tile, tile index = tn * ntm + tm)
-    const int *plan_ptr;   // ntm*ntn + 1 or nullptr
+    // fault plan in the caller's coordinates: CSR by the caller's tile (index gtn * plan_ntm +
+    // gtm over a plan_ntm x plan_ntn grid), entries i, j of the caller's C
+    const int *plan_ptr;   // plan_ntm * plan_ntn + 1 or nullptr
     const long long *plan_i, *plan_j;
     const int *plan_bit;
+    long long plan_ntm, plan_ntn;
     // report
     ReportHdr *rep;
     Correction *rep_entries;
@@ -669,10 +671,14 @@ __global__ void __launch_bounds__(Warps<NWN>::NT + Warps<NWN>::PT, NWN == 2 ? 2 
             mbar_init(&full_bar[s], 1 + (ALL_TMA ? 0 : PT));
             mbar_init(&empty_bar[s], NT / 32);  // one arrival per MMA warp
         }
-        mbar_init(&norm_bar, PT - 32);  // producer warps 1..3 (NWN = 4)
+        if (NWN == 4 && FT) mbar_init(&norm_bar, PT - 32);  // producer warps 1..3
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
+    // PAIR: every thread arrives on the cluster barrier now and the MMA threads wait on it
+    // before the first distributed-shared-memory store, so the peer CTA is known to have
+    // started (the programming model's requirement for DSMEM access)
+    if (PAIR) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
 
     if (warp >= NT / 32) {
         // ------------------------------------------------------------ producer warpgroup
@@ -945,11 +951,12 @@ __global__ void __launch_bounds__(Warps<NWN>::NT + Warps<NWN>::PT, NWN == 2 ? 2 
         bar_mma();
     }
     // fault injection (test harness): flip accumulator bits of planned elements of this tile
-    if (g.plan_ptr) {
-        const int tix = (int)(tn * ntm + tm);
+    const long long gtm = tm + g.off_i / BM, gtn = tn + g.off_j / BN;  // the caller's tile
+    if (g.plan_ptr && gtm < g.plan_ntm && gtn < g.plan_ntn) {
+        const long long tix = gtn * g.plan_ntm + gtm;
         const int lo = g.plan_ptr[tix], hi = g.plan_ptr[tix + 1];
         for (int f = lo; f < hi; f++) {
-            const long long li = g.plan_i[f] - m0, lj = g.plan_j[f] - n0;
+            const long long li = g.plan_i[f] - g.off_i - m0, lj = g.plan_j[f] - g.off_j - n0;
             const int bit = g.plan_bit[f];
 #pragma unroll
             for (int a = 0; a < FM; a++)
@@ -1122,6 +1129,7 @@ __global__ void __launch_bounds__(Warps<NWN>::NT + Warps<NWN>::PT, NWN == 2 ? 2 
         // one cluster barrier per tile: the columns are verified before the exchange, so the
         // column-flag count travels with the row partial sums
         const unsigned peer = (unsigned)(half ^ 1);
+        asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");  // peer started (arrived at entry)
         for (int qq = tid; qq < BM + BNT; qq += NT) {
             if (qq < BM) {
 #pragma unroll

@@ -187,7 +187,8 @@ def test_encode_spec_examples():
     crow, ccol, c0row, c0col = oracle.ref_checksums(
         "N", "N", 2, 1.0, Z, 2, Z, 2, cc["beta"], C0, 2, 0, 2, 0, 2, np.zeros(2), np.zeros(2))
     assert ccol.tolist() == cc["c_col"] and crow.tolist() == cc["c_row"]
-    assert c0row.tolist() == [2.0, 2.0] and c0col.tolist() == [2.0, 2.0]
+    # R4k: n * up(max |C0|), up(1.0) = 1 + 2^-20 (high word 0x3ff00000 + 1, low word 0)
+    assert c0row.tolist() == [2.0 * (1 + 2.0 ** -20)] * 2 and c0col.tolist() == [2.0 * (1 + 2.0 ** -20)] * 2
 
 
 @pytest.mark.parametrize("tA", ["N", "T"])
@@ -250,10 +251,155 @@ def test_checksum_invariants_exact(tA, tB):
                 i0, i1, j0, j1, ac, br)
             for i in range(i0, i1):
                 assert crow[i - i0] == float(sum(exact[i][j] for j in range(j0, j1)))
-                want = sum(abs(d["C"][i, j]) for j in range(j0, j1)) if beta != 0 else 0.0
+                want = c0_bound_indep([d["C"][i, j] for j in range(j0, j1)]) if beta != 0 else 0.0
                 assert c0row[i - i0] == want
             for j in range(j0, j1):
                 assert ccol[j - j0] == float(sum(exact[i][j] for i in range(i0, i1)))
+                want = c0_bound_indep([d["C"][i, j] for i in range(i0, i1)]) if beta != 0 else 0.0
+                assert c0col[j - j0] == want
+
+
+def up_indep(m: float) -> float:
+    """Smallest double with a zero low 32-bit word strictly above |m| (struct, not the oracle)."""
+    bits = struct.unpack("<Q", struct.pack("<d", abs(m)))[0]
+    hi = (bits >> 32) & 0x7FFFFFFF
+    if hi >= 0x7FF00000:
+        return math.inf
+    return struct.unpack("<d", struct.pack("<Q", (hi + 1) << 32))[0]
+
+
+def c0_bound_indep(vals) -> float:
+    """Reading R4k: n * up(max |v|) (NaN / Inf -> +Inf)."""
+    if any(math.isnan(v) or math.isinf(v) for v in vals):
+        return math.inf
+    return len(vals) * up_indep(max(abs(v) for v in vals))
+
+
+def test_c0_bounds_nonuniform_integers():
+    """The |C0| terms of the threshold (c0row, c0col) on non-uniform integer data with a
+    distinct maximum per row and column, negatives and zeros: equal to the independent
+    definition and >= the exact sums sum |C0| they bound (a wrong index, range or a row/column
+    swap changes the maxima here)."""
+    rng = np.random.default_rng(43)
+    M, N = 13, 11
+    C0 = np.asfortranarray(rng.integers(-9, 10, size=(M, N)).astype(np.float64))
+    C0[3, :] = 0.0
+    C0[:, 5] *= 1000.0
+    C0[7, 2] = -2.0 ** 40
+    Z = np.asfortranarray(np.zeros((M, N)))
+    for (i0, i1, j0, j1) in [(0, M, 0, N), (2, 9, 1, 7), (12, 13, 4, 11)]:
+        _, _, c0row, c0col = oracle.ref_checksums("N", "N", 1, 1.0, Z, M, Z, 1, 0.5, C0, M,
+                                                  i0, i1, j0, j1, np.zeros(1), np.zeros(1))
+        for i in range(i0, i1):
+            row = [float(C0[i, j]) for j in range(j0, j1)]
+            assert c0row[i - i0] == c0_bound_indep(row)
+            assert c0row[i - i0] >= sum(abs(v) for v in row)
+        for j in range(j0, j1):
+            col = [float(C0[i, j]) for i in range(i0, i1)]
+            assert c0col[j - j0] == c0_bound_indep(col)
+            assert c0col[j - j0] >= sum(abs(v) for v in col)
+    # an Inf in C0 makes the bound infinite; beta = 0 ignores C0 entirely
+    C0[1, 1] = math.inf
+    _, _, c0row, c0col = oracle.ref_checksums("N", "N", 1, 1.0, Z, M, Z, 1, 2.0, C0, M,
+                                              0, M, 0, N, np.zeros(1), np.zeros(1))
+    assert math.isinf(c0row[1]) and math.isinf(c0col[1]) and math.isfinite(c0row[0])
+    _, _, c0row, c0col = oracle.ref_checksums("N", "N", 1, 1.0, Z, M, Z, 1, 0.0, C0, M,
+                                              0, M, 0, N, np.zeros(1), np.zeros(1))
+    assert (c0row == 0).all() and (c0col == 0).all()
+
+
+def tau_exact(d, tA, tB, K, alpha, beta, i0, i1, j0, j1, i=None, j=None):
+    """Row (i given) or column (j given) threshold of reading R4/R4k from exact sums."""
+    a, b = op_exact(d["A"], tA), op_exact(d["B"], tB)
+    if i is not None:
+        n = j1 - j0
+        rowabs = sum(abs(a[i][k]) for k in range(K))
+        bmax = max(sum(abs(b[k][jj]) for jj in range(j0, j1)) for k in range(K))
+        c0 = Fraction(c0_bound_indep([float(d["C"][i, jj]) for jj in range(j0, j1)])) if beta else 0
+        return 4 * Fraction(U) * (K + n + 3) * (abs(Fraction(alpha)) * rowabs * bmax + abs(Fraction(beta)) * c0)
+    m = i1 - i0
+    colabs = sum(abs(b[k][j]) for k in range(K))
+    amax = max(sum(abs(a[ii][k]) for ii in range(i0, i1)) for k in range(K))
+    c0 = Fraction(c0_bound_indep([float(d["C"][ii, j]) for ii in range(i0, i1)])) if beta else 0
+    return 4 * Fraction(U) * (K + m + 3) * (abs(Fraction(alpha)) * amax * colabs + abs(Fraction(beta)) * c0)
+
+
+@pytest.mark.parametrize("tA,tB", [("N", "T"), ("T", "N")])
+def test_threshold_pinned_within_one_percent(tA, tB):
+    """tau (reading R4/R4k) is pinned to +-1 %: an additive perturbation of 0.99 tau is not
+    flagged, one of 1.01 tau is, separately for the row and the column threshold (computed
+    here from exact sums).  A tau off by a factor >= 1.01 either way, a dropped term or a
+    row / column mix-up fails."""
+    rng = np.random.default_rng(47)
+    M, N, K = 40, 36, 50
+    alpha, beta = 1.5, -0.5
+    w = syn.Workload("t", M, N, K, tA, tB, alpha, beta, "uniform", True, int(rng.integers(1 << 30)))
+    d = syn.make_inputs(w)
+    clean = clean_tile(d, tA, tB, M, N, K, alpha, beta)
+    for trial in range(3):
+        i, j = int(rng.integers(M)), int(rng.integers(N))
+        tr = float(tau_exact(d, tA, tB, K, alpha, beta, 0, M, 0, N, i=i))
+        tc = float(tau_exact(d, tA, tB, K, alpha, beta, 0, M, 0, N, j=j))
+        for delta in (0.99 * tr, 1.01 * tr, 0.99 * tc, 1.01 * tc):
+            for sign in (1.0, -1.0):
+                Ct = clean.copy(order="F")
+                Ct[i, j] += sign * delta
+                rep, st = oracle.verify_tile(tA, tB, K, alpha, d["A"], d["lda"], d["B"], d["ldb"], beta,
+                                             d["C"], d["ldc"], 0, M, 0, N, 0, 0, Ct)
+                assert st.rows_flagged == (1 if delta > tr else 0), (delta / tr, trial)
+                assert st.cols_flagged == (1 if delta > tc else 0), (delta / tc, trial)
+                if delta > min(tr, tc):  # located (single flag pair or candidate recompute)
+                    assert [(r["i"], r["j"]) for r in rep] == [(i, j)]
+                    assert np.array_equal(Ct, clean)
+                else:
+                    assert rep == []
+
+
+def flip_indep(x: float, bit: int) -> float:
+    b = struct.unpack("<Q", struct.pack("<d", x))[0] ^ (1 << bit)
+    return struct.unpack("<d", struct.pack("<Q", b))[0]
+
+
+def test_subthreshold_flip_window():
+    """Reading R10: a flip whose change is below the row and column thresholds is not
+    flagged (indistinguishable from rounding) and stays in C, within tau of
+    the fault-free value; flips of the same element above twice the thresholds are located and
+    corrected.  Sweeps every bit 0..62 of one element and checks each against exact tau."""
+    rng = np.random.default_rng(53)
+    M, N, K = 48, 40, 64
+    alpha, beta = 1.5, -0.5
+    w = syn.Workload("t", M, N, K, "N", "T", alpha, beta, "uniform", True, 4242)
+    d = syn.make_inputs(w)
+    clean = clean_tile(d, "N", "T", M, N, K, alpha, beta)
+    i, j = 17, 23
+    a, b = op_exact(d["A"], "N"), op_exact(d["B"], "T")
+    acc = float(sum(a[i][k] * b[k][j] for k in range(K)))  # |exact - fl(acc)| << tau
+    tr = float(tau_exact(d, "N", "T", K, alpha, beta, 0, M, 0, N, i=i))
+    tc = float(tau_exact(d, "N", "T", K, alpha, beta, 0, M, 0, N, j=j))
+    tmin = min(tr, tc)
+    below = above = 0
+    for bit in range(63):
+        delta = abs(alpha * (flip_indep(acc, bit) - acc))
+        if 0.5 * tmin < delta < 2.0 * max(tr, tc):
+            continue  # within a factor 2 of a threshold: pinned by the 1 % test above
+        C = d["C"].copy(order="F")
+        rep, st = oracle.abft_dgemm("N", "T", M, N, K, alpha, d["A"], d["lda"], d["B"], d["ldb"], beta,
+                                    C, d["ldc"], tile_m=64, tile_n=64,
+                                    faults=(np.array([i]), np.array([j]), np.array([bit])))
+        mask = np.ones_like(C, dtype=bool)
+        mask[i, j] = False
+        assert np.array_equal(C[mask], clean[mask])
+        if delta <= 0.5 * tmin:
+            below += 1
+            assert rep == [] and st.tiles_flagged == 0
+            assert abs(C[i, j] - clean[i, j]) <= tr and abs(C[i, j] - clean[i, j]) <= tc
+            if delta > 4 * K * U * abs(alpha) * 64:  # above the per-element bound: really stays
+                assert C[i, j] != clean[i, j]
+        else:
+            above += 1
+            assert [(r["i"], r["j"], r["kind"]) for r in rep] == [(i, j, 1)]
+            assert C[i, j] == clean[i, j]
+    assert below >= 10 and above >= 20
 
 
 # ----------------------------------------------------------------- verify / locate / correct
