@@ -258,6 +258,109 @@ def test_blocked_calls_with_offsets_and_append(ft, split):
     assert_close(w, d, C, C_ref)
 
 
+def test_blocked_calls_growing_workspace(ft):
+    """Column blocks of increasing width after ftblas_release(), later blocks asking to reuse
+    the A encoding: the workspace grows on the second and third call (free + malloc), so the
+    cached encoding must be dropped and A encoded again.  Report and C must
+    equal the oracle's for the whole problem."""
+    w = syn.Workload("grow", 384, 1024, 96, "N", "N", 1.0, -1.0, "uniform", True, seed=29)
+    d = syn.make_inputs(w)
+    plan = syn.fault_plan(w.M, w.N, 7, 13)
+    A_t, pA = to_dev(d["A"]); B_t, pB = to_dev(d["B"]); C_t, pC = to_dev(d["C"])
+    ft.ftblas_release()
+    ft.ftblas_set_fault_plan(*plan)
+    ft.ftblas_report_reset()
+    for q, (c0, c1) in enumerate([(0, 128), (128, 384), (384, 1024)]):
+        ft.ftblas_dgemm_ex("N", "N", w.M, c1 - c0, w.K, w.alpha, pA, d["lda"], pB + 8 * c0 * d["ldb"],
+                           d["ldb"], w.beta, pC + 8 * c0 * d["ldc"], d["ldc"], 0, c0, q > 0, reuse_a=q > 0)
+    rep = ft.ftblas_report_fetch(ft.Report(64))
+    ft.ftblas_clear_fault_plan()
+    C = from_dev(C_t, d["C"])
+    C_ref, orep, st = run_oracle(w, d, plan)
+    assert rep.count == st.count == 7 and rep.tiles_flagged == st.tiles_flagged
+    assert report_key(rep.entries()) == report_key(orep)
+    assert_close(w, d, C, C_ref)
+
+
+def _flip(x: float, bit: int) -> float:
+    import struct
+    b = struct.unpack("<Q", struct.pack("<d", x))[0] ^ (1 << bit)
+    return struct.unpack("<d", struct.pack("<Q", b))[0]
+
+
+def test_gpu_subthreshold_flip_matches_oracle(ft):
+    """Reading R10: flips too small for the round-off threshold (low mantissa bits) are left in
+    C by both sides -- identical (empty) reports, C within the R9 tolerance of the oracle's C
+    (which keeps the same flipped value) -- while large flips in the same run are corrected."""
+    w = syn.Workload("sub", 256, 256, 200, "N", "T", 1.5, -0.5, "uniform", True, seed=61)
+    d = syn.make_inputs(w)
+    # one flip per tile: bits 8..20 (far below tau ~ 1e-9 for |C| ~ 5) in three tiles, bit 50
+    # (far above) in the fourth
+    plan = (np.array([5, 140, 20, 200], np.int64), np.array([7, 30, 150, 222], np.int64),
+            np.array([8, 14, 20, 50], np.int32))
+    C_gpu, rep = run_gpu(ft, w, d, plan=plan)
+    C_ref, orep, st = run_oracle(w, d, plan)
+    assert report_key(rep.entries()) == report_key(orep)
+    assert [(e["i"], e["j"]) for e in rep.entries()] == [(200, 222)]
+    assert_close(w, d, C_gpu, C_ref)
+    # the sub-threshold flips really stayed (their change exceeds the R9 tolerance): compare
+    # with the oracle's fault-free C
+    C_clean, _, _ = run_oracle(w, d)
+    ab = abs_product(w, d)
+    for i, j, bit in zip(*[p.tolist() for p in plan]):
+        tol = 4 * (w.K + 2) * 2.0 ** -53 * (abs(w.alpha) * ab[i, j] + abs(w.beta) * abs(d["C"][i, j]))
+        if bit < 40:
+            assert abs(C_gpu[i, j] - C_clean[i, j]) > tol, (i, j, bit)
+        else:
+            assert abs(C_gpu[i, j] - C_clean[i, j]) <= tol
+
+
+def test_gpu_c0_bound_window_matches_oracle(ft):
+    """Reading R4k: when the |beta| |C0| term dominates the threshold, flips whose change lies
+    between the exact-sum threshold (sum |C0|) and the bound actually used (n up(max |C0|)) are
+    not flagged -- by the kernel and, since round 2, by the oracle alike (round 1's oracle used
+    the sum and flagged them); flips above the bound are corrected by both."""
+    w = syn.Workload("win", 256, 256, 64, "N", "N", 1.0, 1.0, "uniform", True, seed=67)
+    d = syn.make_inputs(w)
+    scale = 1e-4  # operands small: |alpha| |A||B| << |beta| |C0| in the threshold
+    d["A"] = np.asfortranarray(d["A"] * scale)
+    d["B"] = np.asfortranarray(d["B"] * scale)
+    opA, opB = d["A"], d["B"]
+    acc = opA @ opB
+    U = 2.0 ** -53
+    K = w.K
+    picks = []
+    for (tm, tn) in [(0, 0), (0, 1), (1, 0), (1, 1)]:
+        r0, c0 = 128 * tm, 128 * tn
+        tile_c0 = np.abs(d["C"][r0:r0 + 128, c0:c0 + 128])
+        rng = np.random.default_rng(tm * 2 + tn)
+        for _ in range(2000):
+            i, j = r0 + int(rng.integers(128)), c0 + int(rng.integers(128))
+            rowabs = np.abs(opA[i, :]).sum()
+            bmax = np.abs(opB[:, c0:c0 + 128]).sum(axis=1).max()
+            colabs = np.abs(opB[:, j]).sum()
+            amax = np.abs(opA[r0:r0 + 128, :]).sum(axis=0).max()
+            t_sum_r = 4 * U * (K + 131) * (rowabs * bmax + tile_c0[i - r0, :].sum())
+            t_max_r = 4 * U * (K + 131) * (rowabs * bmax + 128 * tile_c0[i - r0, :].max())
+            t_sum_c = 4 * U * (K + 131) * (amax * colabs + tile_c0[:, j - c0].sum())
+            t_max_c = 4 * U * (K + 131) * (amax * colabs + 128 * tile_c0[:, j - c0].max())
+            lo, hi = 1.1 * max(t_sum_r, t_sum_c), 0.9 * min(t_max_r, t_max_c)
+            bits = [b for b in range(53) if lo < abs(_flip(acc[i, j], b) - acc[i, j]) < hi]
+            if bits:
+                picks.append((i, j, bits[0]))
+                break
+    assert len(picks) >= 3, picks
+    big = (60, 60, 55)  # and one flip far above every threshold, in tile (0, 0)
+    plan = (np.array([p[0] for p in picks] + [big[0]], np.int64),
+            np.array([p[1] for p in picks] + [big[1]], np.int64),
+            np.array([p[2] for p in picks] + [big[2]], np.int32))
+    C_gpu, rep = run_gpu(ft, w, d, plan=plan)
+    C_ref, orep, st = run_oracle(w, d, plan)
+    assert report_key(rep.entries()) == report_key(orep)
+    assert [(e["i"], e["j"]) for e in rep.entries()] == [(60, 60)]
+    assert_close(w, d, C_gpu, C_ref)
+
+
 def test_ex_argument_errors(ft):
     with pytest.raises(ft.FtblasError):
         ft.ftblas_dgemm_ex("N", "N", 4, 4, 4, 1.0, 0, 4, 0, 4, 0.0, 0, 4, 64, 0)
@@ -290,66 +393,115 @@ def sampled_check(w, d, C_gpu, n=300, seed=0, extra=()):
         assert abs(C_gpu[i, j] - ref) <= tol, (i, j, C_gpu[i, j], ref)
 
 
-def tile_mask(w, plan, limit=None):
-    ntm, ntn = -(-w.M // 128), -(-w.N // 128)
-    mask = np.zeros(ntm * ntn, np.uint8)
-    sel = list(zip(plan[0].tolist(), plan[1].tolist()))[:limit]
-    for i, j in sel:
-        mask[(j // 128) * ntm + i // 128] = 1
-    return mask, sel
+_PAR = {}
 
 
-def check_full_config(ft, w, oracle_tiles=None):
+def _tile_plan(plan, r0, r1, c0, c1):
+    if plan is None:
+        return None
+    i, j, bit = plan
+    m = (i >= r0) & (i < r1) & (j >= c0) & (j < c1)
+    return (i[m] - r0, j[m] - c0, bit[m])
+
+
+def _oracle_tile(t):
+    """The unchanged oracle on one verification tile as a stand-alone problem (a tile's
+    verification reads only op(A) rows I, op(B) columns J and the C0 tile), shifted back to
+    the caller's coordinates."""
+    w, d, plan = _PAR["w"], _PAR["d"], _PAR["plan"]
+    tm, tn = t
+    r0, r1 = 128 * tm, min(w.M, 128 * tm + 128)
+    c0, c1 = 128 * tn, min(w.N, 128 * tn + 128)
+    A = d["A"][r0:r1, :] if w.transA == "N" else d["A"][:, r0:r1]
+    B = d["B"][:, c0:c1] if w.transB == "N" else d["B"][c0:c1, :]
+    C = np.asfortranarray(d["C"][r0:r1, c0:c1].copy())
+    lda = d["lda"]
+    ldb = d["ldb"]
+    sub = _tile_plan(plan, r0, r1, c0, c1)
+    rep, st = oracle.abft_dgemm(w.transA, w.transB, r1 - r0, c1 - c0, w.K, w.alpha, A, lda, B, ldb,
+                                w.beta, C, r1 - r0, faults=sub, cap=64)
+    ents = [dict(e, tile_m=tm, tile_n=tn, i=e["i"] + r0, j=e["j"] + c0) for e in rep]
+    return tm, tn, C, ents
+
+
+def oracle_tiles(w, d, plan, tiles):
+    """Oracle results of the listed (tm, tn) tiles, in parallel over the host cores (fork:
+    the inputs are shared copy-on-write)."""
+    import multiprocessing as mp
+    import os
+    _PAR.update(w=w, d=d, plan=plan)
+    procs = max(1, min(len(tiles), os.cpu_count() or 1))
+    if procs == 1:
+        return [_oracle_tile(t) for t in tiles]
+    with mp.get_context("fork").Pool(procs) as pool:
+        return pool.map(_oracle_tile, tiles, chunksize=1)
+
+
+def check_tiles(w, d, C_gpu, results):
+    opA = d["A"] if w.transA == "N" else d["A"].T
+    opB = d["B"] if w.transB == "N" else d["B"].T
+    for tm, tn, Ct, _ in results:
+        r0, c0 = 128 * tm, 128 * tn
+        r1, c1 = r0 + Ct.shape[0], c0 + Ct.shape[1]
+        ab = np.abs(opA[r0:r1, :]) @ np.abs(opB[:, c0:c1])
+        cc = np.abs(d["C"][r0:r1, c0:c1]) if w.beta != 0 else 0.0
+        tol = gemm_bound(w.K, w.alpha, w.beta, ab, cc)
+        bad = ~(np.abs(C_gpu[r0:r1, c0:c1] - Ct) <= tol)
+        assert not bad.any(), (tm, tn, int(bad.sum()))
+
+
+def check_full_config(ft, w, clean_tiles=64):
+    """Full-size config: the fault-free run on `clean_tiles` random tiles and the injected run
+    on EVERY faulty tile plus the same clean tiles are compared with the oracle tile by tile
+    (whole tiles, elementwise bound; reports bit-exact on the faulty tiles), plus sampled
+    single-element dots anywhere."""
     d = syn.make_inputs(w)
     plan = syn.fault_plan(w.M, w.N, w.n_flips, w.seed)
-    # fault-free run: no report, sampled elements within tolerance
+    ntm, ntn = -(-w.M // 128), -(-w.N // 128)
+    faulty = sorted({(int(i) // 128, int(j) // 128) for i, j in zip(plan[0], plan[1])})
+    rng = np.random.default_rng(w.seed + 1000)
+    clean = []
+    while len(clean) < min(clean_tiles, ntm * ntn - len(faulty)):
+        t = (int(rng.integers(ntm)), int(rng.integers(ntn)))
+        if t not in faulty and t not in clean:
+            clean.append(t)
+    # fault-free run: no report; the clean tiles equal the oracle's
     C_clean, rep0 = run_gpu(ft, w, d)
     assert rep0.count == 0 and rep0.tiles_flagged == 0
+    res_clean = oracle_tiles(w, d, None, clean)
+    check_tiles(w, d, C_clean, res_clean)
     sampled_check(w, d, C_clean, n=100)
-    # injected run
+    # injected run: every planned flip located and corrected; faulty tiles vs the oracle
     C_gpu, rep = run_gpu(ft, w, d, plan=plan)
     got = report_key(rep.entries())
     assert rep.count == w.n_flips
     assert sorted((g[2], g[3]) for g in got) == sorted(zip(plan[0].tolist(), plan[1].tolist()))
-    # oracle on the faulty tiles it can afford
-    mask, sel = tile_mask(w, plan, oracle_tiles)
-    C_or, orep, st = run_oracle(w, d, plan, tiles_only=mask)
-    sel_tiles = {(i // 128, j // 128) for i, j in sel}
-    assert report_key(orep) == [g for g in got if (g[0], g[1]) in sel_tiles]
-    ntm = -(-w.M // 128)
-    for (i, j) in sel:
-        tm, tn = i // 128, j // 128
-        r0, r1 = tm * 128, min(w.M, tm * 128 + 128)
-        c0, c1 = tn * 128, min(w.N, tn * 128 + 128)
-        sub_w = w
-        ab = None
-        # elementwise tolerance on the whole tile
-        opA = d["A"] if w.transA == "N" else d["A"].T
-        opB = d["B"] if w.transB == "N" else d["B"].T
-        ab = np.abs(opA[r0:r1, :]) @ np.abs(opB[:, c0:c1])
-        cc = np.abs(d["C"][r0:r1, c0:c1]) if w.beta != 0 else 0.0
-        tol = gemm_bound(w.K, w.alpha, w.beta, ab, cc)
-        assert (np.abs(C_gpu[r0:r1, c0:c1] - C_or[r0:r1, c0:c1]) <= tol).all()
-        assert (np.abs(C_gpu[r0:r1, c0:c1] - C_clean[r0:r1, c0:c1]) <= 2 * tol).all()
+    res = oracle_tiles(w, d, plan, faulty)
+    assert report_key([e for r in res for e in r[3]]) == got
+    check_tiles(w, d, C_gpu, res)
+    # the clean tiles are untouched by the injection (bitwise the fault-free run's)
+    for tm, tn, Ct, _ in res_clean:
+        sl = (slice(128 * tm, 128 * tm + Ct.shape[0]), slice(128 * tn, 128 * tn + Ct.shape[1]))
+        assert np.array_equal(C_gpu[sl], C_clean[sl])
     sampled_check(w, d, C_gpu, n=100, seed=1, extra=list(zip(plan[0].tolist(), plan[1].tolist()))[:50])
 
 
 def test_config1_4096_tn(ftd):
-    check_full_config(ftd, syn.CONFIGS[1], oracle_tiles=100)
+    check_full_config(ftd, syn.CONFIGS[1])
 
 
 def test_config2_rank_k_update(ftd):
-    check_full_config(ftd, syn.CONFIGS[2], oracle_tiles=32)
+    check_full_config(ftd, syn.CONFIGS[2])
 
 
 def test_config3_16384(ftd):
-    check_full_config(ftd, syn.CONFIGS[3], oracle_tiles=6)
+    check_full_config(ftd, syn.CONFIGS[3])
 
 
 def test_config4_32768x16384(ftd):
     """configs[4] is quoted for an 8-GPU row-block shard; each shard runs the single-GPU call,
     so the whole problem on one GPU (17 GB of operands) checks the same kernels at full size."""
-    check_full_config(ftd, syn.CONFIGS[4], oracle_tiles=4)
+    check_full_config(ftd, syn.CONFIGS[4], clean_tiles=16)
 
 
 def test_zero_fault_transparency_and_no_false_positives(ft):
