@@ -294,10 +294,18 @@ def test_gpu_subthreshold_flip_matches_oracle(ft):
     (which keeps the same flipped value) -- while large flips in the same run are corrected."""
     w = syn.Workload("sub", 256, 256, 200, "N", "T", 1.5, -0.5, "uniform", True, seed=61)
     d = syn.make_inputs(w)
-    # one flip per tile: bits 8..20 (far below tau ~ 1e-9 for |C| ~ 5) in three tiles, bit 50
-    # (far above) in the fourth
-    plan = (np.array([5, 140, 20, 200], np.int64), np.array([7, 30, 150, 222], np.int64),
-            np.array([8, 14, 20, 50], np.int32))
+    # one flip per tile: in three tiles a low mantissa bit whose change is >= 10x the R9
+    # tolerance but <= 1e-10 (about 1/10 of the row threshold tau ~ 1e-9 here), bit 50 (far
+    # above tau) in the fourth
+    ab = abs_product(w, d)
+    ii, jj, bits = [5, 140, 20, 200], [7, 30, 150, 222], []
+    for i, j in zip(ii[:3], jj[:3]):
+        acc = oracle.dot(w.transA, w.transB, w.K, d["A"], d["lda"], d["B"], d["ldb"], i, j)
+        tol = 4 * (w.K + 2) * 2.0 ** -53 * (abs(w.alpha) * ab[i, j] + abs(w.beta) * abs(d["C"][i, j]))
+        ok = [b for b in range(52) if 10 * tol <= abs(w.alpha * (_flip(acc, b) - acc)) <= 1e-10]
+        assert ok, (i, j)
+        bits.append(ok[-1])
+    plan = (np.array(ii, np.int64), np.array(jj, np.int64), np.array(bits + [50], np.int32))
     C_gpu, rep = run_gpu(ft, w, d, plan=plan)
     C_ref, orep, st = run_oracle(w, d, plan)
     assert report_key(rep.entries()) == report_key(orep)
@@ -306,7 +314,6 @@ def test_gpu_subthreshold_flip_matches_oracle(ft):
     # the sub-threshold flips really stayed (their change exceeds the R9 tolerance): compare
     # with the oracle's fault-free C
     C_clean, _, _ = run_oracle(w, d)
-    ab = abs_product(w, d)
     for i, j, bit in zip(*[p.tolist() for p in plan]):
         tol = 4 * (w.K + 2) * 2.0 ** -53 * (abs(w.alpha) * ab[i, j] + abs(w.beta) * abs(d["C"][i, j]))
         if bit < 40:
