@@ -197,6 +197,8 @@ def main():
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo: functional check of the multi-rank "
                          "path on fewer GPUs than ranks; not a performance configuration)")
+    ap.add_argument("--tiles", default="auto", choices=["auto", "full", "pair", "ws"],
+                    help="CTA tiling policy of the GEMM kernels (ftblas_set_tile_policy)")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     args = ap.parse_args()
@@ -222,6 +224,7 @@ def main():
     stream = torch.cuda.current_stream()
     fb.ftblas_set_stream(stream)
     fb.ftblas_set_checksum_mode("gemm")
+    fb.ftblas_set_tile_policy(args.tiles)
 
     def barrier():
         if world > 1:

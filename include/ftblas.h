@@ -167,6 +167,7 @@ int ftblas_get_checksum_mode(void);
 #define FTBLAS_TILES_AUTO 0
 #define FTBLAS_TILES_FULL 1
 #define FTBLAS_TILES_PAIR 2
+#define FTBLAS_TILES_WS 3
 int ftblas_set_tile_policy(int policy);
 int ftblas_get_tile_policy(void);
 

@@ -5,6 +5,7 @@
 // launches on the caller's stream, report readback.  All arithmetic of the hot
 // path runs in the kernels of ftblas_kernels.cuh.
 #include "ftblas_kernels.cuh"
+#include "ftblas_ws.cuh"
 #include "../../include/ftblas.h"
 
 #include <algorithm>
@@ -177,6 +178,36 @@ cudaError_t launch_gemm(bool kca, bool kcb, bool tma, const GemmArgs &g, const C
                         const CUtensorMap &mb, long long tiles, cudaStream_t s) {
     // 8 instantiations per mode and tile width: transpose layout x (TMA | cp.async fallback)
 #define L(a, b, c) if (kca == a && kcb == b && tma == c) return launch_gemm_t<a, b, c, MODE, NWN>(g, ma, mb, tiles, s)
+    L(false, true, true); L(false, false, true); L(true, true, true); L(true, false, true);
+    L(false, true, false); L(false, false, false); L(true, true, false); L(true, false, false);
+#undef L
+    return cudaErrorInvalidValue;
+}
+
+int sm_count() {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    return n;
+}
+
+// Persistent warp-specialized kernel (ftblas_ws.cuh): one CTA per SM over all tiles.
+template <bool KCA, bool KCB, bool TMA, bool FT>
+cudaError_t launch_ws_t(const GemmArgs &g, const CUtensorMap &ma, const CUtensorMap &mb, long long tiles,
+                        cudaStream_t s) {
+    auto kern = gemm_ws_kernel<KCA, KCB, TMA, FT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_SMEM);
+    if (e != cudaSuccess) return e;
+    const unsigned grid = (unsigned)std::min<long long>(tiles, sm_count());
+    kern<<<grid, WS_THREADS, WS_SMEM, s>>>(g, ma, mb);
+    ctx().launches++;
+    return cudaGetLastError();
+}
+
+template <bool FT>
+cudaError_t launch_ws(bool kca, bool kcb, bool tma, const GemmArgs &g, const CUtensorMap &ma, const CUtensorMap &mb,
+                      long long tiles, cudaStream_t s) {
+#define L(a, b, c) if (kca == a && kcb == b && tma == c) return launch_ws_t<a, b, c, FT>(g, ma, mb, tiles, s)
     L(false, true, true); L(false, false, true); L(true, true, true); L(true, false, true);
     L(false, true, false); L(false, false, false); L(true, true, false); L(true, false, false);
 #undef L
@@ -412,8 +443,9 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
     // the other) when the per-tile mainloop is short, 128 x 128 CTAs otherwise; the fused
     // checksum mode always uses 128 x 128
     const bool fused = ft && c.checksum_mode == FTBLAS_CHECKSUM_FUSED;
-    const bool pair = !fused && (c.tile_policy == FTBLAS_TILES_PAIR ||
-                                 (c.tile_policy == FTBLAS_TILES_AUTO && K <= c.pair_kmax));
+    const bool ws = !fused && c.tile_policy == FTBLAS_TILES_WS;
+    const bool pair = !fused && !ws && (c.tile_policy == FTBLAS_TILES_PAIR ||
+                                        (c.tile_policy == FTBLAS_TILES_AUTO && K <= c.pair_kmax));
     const Staging stg = make_staging(A, lda, M, kca, B, ldb, N, kcb, K, alpha, pair ? 64u : 128u);
     Ctx::Rec rec{};
     if (c.profiling) {
@@ -547,7 +579,7 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
             CK(cudaMemsetAsync(Rpre, 0, (oS - oR + (size_t)spS * ntm * N) * sizeof(double), c.stream), "checksum zero");
             (void)nRS;
         }
-        if (pre && pair) {
+        if (pre && (pair || ws)) {
             // per-row / per-column side data of the verification: partials summed once (the
             // pair-tile producers copy them; 128 x 128 tiles sum the partials in the producer)
             FinArgs fa{};
@@ -564,7 +596,9 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
             CK(cudaGetLastError(), "side_finalize_kernel launch");
         }
         if (c.profiling) CK(cudaEventRecord(rec.e1, c.stream), "event");
-        if (pre)
+        if (pre && ws)
+            CK((launch_ws<true>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream)), "gemm_ws_kernel<FT> launch");
+        else if (pre)
             CK((pair ? launch_gemm<MODE_FT_PRE, 2>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream)
                      : launch_gemm<MODE_FT_PRE, 4>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream)),
                "gemm_kernel<FT> launch");
@@ -573,9 +607,12 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
                "gemm_kernel<FT> launch");
     } else {
         if (c.profiling) CK(cudaEventRecord(rec.e1, c.stream), "event");
-        CK((pair ? launch_gemm<MODE_NOFT, 2>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream)
-                 : launch_gemm<MODE_NOFT, 4>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream)),
-           "gemm_kernel launch");
+        if (ws)
+            CK((launch_ws<false>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream)), "gemm_ws_kernel launch");
+        else
+            CK((pair ? launch_gemm<MODE_NOFT, 2>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream)
+                     : launch_gemm<MODE_NOFT, 4>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream)),
+               "gemm_kernel launch");
     }
     if (c.profiling) {
         CK(cudaEventRecord(rec.e2, c.stream), "event");
@@ -830,7 +867,8 @@ int ftblas_set_checksum_mode(int mode) {
 int ftblas_get_checksum_mode(void) { return ctx().checksum_mode; }
 
 int ftblas_set_tile_policy(int policy) {
-    if (policy != FTBLAS_TILES_AUTO && policy != FTBLAS_TILES_FULL && policy != FTBLAS_TILES_PAIR)
+    if (policy != FTBLAS_TILES_AUTO && policy != FTBLAS_TILES_FULL && policy != FTBLAS_TILES_PAIR &&
+        policy != FTBLAS_TILES_WS)
         return arg_fail(1, "unknown tile policy");
     ctx().tile_policy = policy;
     return 0;

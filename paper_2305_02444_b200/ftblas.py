@@ -91,7 +91,7 @@ EXPORTS = ("ftblas_dgemm", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_rep
            "ftblas_dgemm_ex", "ftblas_report_reset", "ftblas_set_tile_policy",
            "ftblas_get_tile_policy")
 
-TILES = {"auto": 0, "full": 1, "pair": 2}  # FTBLAS_TILES_*
+TILES = {"auto": 0, "full": 1, "pair": 2, "ws": 3}  # FTBLAS_TILES_*
 
 REPORT_APPEND = 1  # FTBLAS_REPORT_APPEND
 REUSE_A_ENCODE = 2  # FTBLAS_REUSE_A_ENCODE
@@ -210,7 +210,7 @@ def ftblas_set_checksum_mode(mode):
 
 
 def ftblas_set_tile_policy(policy):
-    """policy: 'auto' | 'full' | 'pair' or the FTBLAS_TILES_* value."""
+    """policy: 'auto' | 'full' | 'pair' | 'ws' or the FTBLAS_TILES_* value."""
     _check(lib.ftblas_set_tile_policy(TILES.get(policy, policy)))
 
 

@@ -27,8 +27,8 @@ def _lib(mode, tiles="auto"):
     return ftblas
 
 
-@pytest.fixture(params=[("gemm", "pair"), ("gemm", "full"), ("fused", "full")],
-                ids=["gemm-pair", "gemm-full", "fused-full"])
+@pytest.fixture(params=[("gemm", "ws"), ("gemm", "pair"), ("gemm", "full"), ("fused", "full")],
+                ids=["gemm-ws", "gemm-pair", "gemm-full", "fused-full"])
 def ft(request):
     """The library in each checksum mode (checksum GEMMs / fused mainloop checksums) and CTA
     tiling (128 x 64 cluster-pair halves / 128 x 128 tiles)."""
@@ -538,7 +538,7 @@ def test_zero_fault_transparency_and_no_false_positives(ft):
 
 
 @pytest.mark.parametrize("tB", ["N", "T"])
-@pytest.mark.parametrize("tiles", ["pair", "full"])
+@pytest.mark.parametrize("tiles", ["ws", "pair", "full"])
 def test_many_faulted_tiles_leave_neighbours_clean(tB, tiles):
     """Regression: 100 faulted tiles (each with a long single-element recompute) next to clean
     tiles, K deep enough that CTAs of different tiles share SMs for a long time.  Every flag
