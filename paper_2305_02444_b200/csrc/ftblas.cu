@@ -43,6 +43,8 @@ struct Ctx {
     DevBuf ws;            // encode outputs
     DevBuf rep;           // ReportHdr + entries
     long long rep_cap = 1 << 16;
+    DevBuf pend;          // PendingHdr + correction candidates of the persistent kernel
+    long long pend_cap = 1 << 16;
     DevBuf plan_dev;      // fault plan: i, j (caller coordinates), bit, CSR offsets by caller tile
     long long plan_version = 0, plan_uploaded = -1;
     void *plan_host = nullptr;  // pinned staging of the plan upload
@@ -191,17 +193,16 @@ int sm_count() {
     return n;
 }
 
-// Persistent warp-specialized kernel (ftblas_ws.cuh): one CTA per SM over all tiles.
+// Persistent warp-specialized kernel (ftblas_ws.cuh): one CTA per SM over all tiles.  C0 and C
+// move through TMA (box 128 rows x 64 columns, no swizzle, zero fill) when C is 16-byte aligned
+// with an even ldc; otherwise vecC = 0 tells the kernel to use its copy fallback.
+cudaError_t launch_ws_any(const void *kern, GemmArgs g, const CUtensorMap &ma, const CUtensorMap &mb, long long tiles,
+                          cudaStream_t s);
+
 template <bool KCA, bool KCB, bool TMA, bool FT>
 cudaError_t launch_ws_t(const GemmArgs &g, const CUtensorMap &ma, const CUtensorMap &mb, long long tiles,
                         cudaStream_t s) {
-    auto kern = gemm_ws_kernel<KCA, KCB, TMA, FT>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_SMEM);
-    if (e != cudaSuccess) return e;
-    const unsigned grid = (unsigned)std::min<long long>(tiles, sm_count());
-    kern<<<grid, WS_THREADS, WS_SMEM, s>>>(g, ma, mb);
-    ctx().launches++;
-    return cudaGetLastError();
+    return launch_ws_any(reinterpret_cast<const void *>(gemm_ws_kernel<KCA, KCB, TMA, FT>), g, ma, mb, tiles, s);
 }
 
 template <bool FT>
@@ -248,6 +249,34 @@ bool make_operand_map(CUtensorMap *m, const double *X, long long ld, long long M
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
+}
+
+// Tensor map of C for the persistent kernel's epilogue: dims {M, N}, box {128, 64}, no swizzle.
+bool make_c_map(CUtensorMap *m, const double *C, long long ldc, long long M, long long N) {
+    std::memset(m, 0, sizeof(*m));
+    EncodeTiledFn fn = encode_tiled();
+    if (!fn || !C || M <= 0 || N <= 0 || (reinterpret_cast<uintptr_t>(C) & 15) || (ldc & 1)) return false;
+    if (M >= (1ll << 31) || N >= (1ll << 31)) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)N};
+    const cuuint64_t strides[1] = {(cuuint64_t)ldc * 8};
+    const cuuint32_t box[2] = {128u, 64u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(C), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+cudaError_t launch_ws_any(const void *kern, GemmArgs g, const CUtensorMap &ma, const CUtensorMap &mb, long long tiles,
+                          cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_SMEM);
+    if (e != cudaSuccess) return e;
+    CUtensorMap mc;
+    if (!make_c_map(&mc, g.C, g.ldc, g.M, g.N)) g.vecC = 0;
+    const unsigned grid = (unsigned)std::min<long long>(tiles, sm_count());
+    void *args[] = {&g, const_cast<CUtensorMap *>(&ma), const_cast<CUtensorMap *>(&mb), &mc};
+    e = cudaLaunchKernel(kern, dim3(grid), dim3(WS_THREADS), args, WS_SMEM, s);
+    ctx().launches++;
+    return e;
 }
 
 bool vec_ok(const void *p, long long ld) {
@@ -427,6 +456,7 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
     if (rc) return rc;
     if (ft) {
         CK(c.rep.ensure(sizeof(ReportHdr) + c.rep_cap * sizeof(Correction)), "cudaMalloc(report)");
+        CK(c.pend.ensure(sizeof(Pending) + c.pend_cap * sizeof(Pending)), "cudaMalloc(pending)");
     }
     if (M == 0 || N == 0) {
         if (ft && !append) CK(cudaMemsetAsync(c.rep.p, 0, sizeof(ReportHdr), c.stream), "report reset");
@@ -517,6 +547,9 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
         g.rep = c.rep.as<ReportHdr>();
         g.rep_entries = reinterpret_cast<Correction *>(c.rep.as<char>() + sizeof(ReportHdr));
         g.rep_cap = c.rep_cap;
+        g.pend = c.pend.as<PendingHdr>();
+        g.pend_entries = reinterpret_cast<Pending *>(c.pend.as<char>() + sizeof(Pending));
+        g.pend_cap = c.pend_cap;
         g.vecC = vec_ok(C, ldc) ? 1 : 0;
         g.off_i = off_i; g.off_j = off_j;
         if (inject) {
@@ -530,6 +563,7 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
         ea.op[1] = opB;
         ea.K = (alpha == 0.0) ? 0 : K;  // alpha == 0: A, B are not read (encodes are zero)
         ea.Kp = Kp; ea.kper = kper; ea.kch = kch; ea.rep = append ? nullptr : g.rep;
+        ea.pend = g.pend;
         // one launch per layout path (encode_kernel<PATH>): both operands in one launch when
         // they share it; the first launch zeroes the report
         {
@@ -543,6 +577,7 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
                 for (int q = b0; q < b1; q++) tiles = std::max<long long>(tiles, ea.op[q].ntiles);
                 ea.op_base = b0;
                 ea.rep = b0 == 0 ? rep0 : nullptr;
+                ea.pend = b0 == 0 ? g.pend : nullptr;
                 const dim3 grid((unsigned)tiles, (unsigned)kch, (unsigned)(b1 - b0));
                 switch (path_of(ea.op[b0])) {
                     case 0: encode_kernel<0><<<grid, NTHREADS, 0, c.stream>>>(ea); break;
@@ -596,8 +631,17 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
             CK(cudaGetLastError(), "side_finalize_kernel launch");
         }
         if (c.profiling) CK(cudaEventRecord(rec.e1, c.stream), "event");
-        if (pre && ws)
+        if (pre && ws) {
             CK((launch_ws<true>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream)), "gemm_ws_kernel<FT> launch");
+            // the located candidates: recomputed and corrected after the GEMM (ftblas_ws.cuh)
+            const unsigned cb = (unsigned)sm_count();
+            if (!kca && kcb) correct_kernel<false, true><<<cb, CORR_THREADS, 0, c.stream>>>(g);
+            else if (!kca && !kcb) correct_kernel<false, false><<<cb, CORR_THREADS, 0, c.stream>>>(g);
+            else if (kca && kcb) correct_kernel<true, true><<<cb, CORR_THREADS, 0, c.stream>>>(g);
+            else correct_kernel<true, false><<<cb, CORR_THREADS, 0, c.stream>>>(g);
+            c.launches++;
+            CK(cudaGetLastError(), "correct_kernel launch");
+        }
         else if (pre)
             CK((pair ? launch_gemm<MODE_FT_PRE, 2>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream)
                      : launch_gemm<MODE_FT_PRE, 4>(kca, kcb, stg.tma, g, stg.ma, stg.mb, ntm * ntn, c.stream)),
@@ -922,10 +966,21 @@ void ftblas_tile_shape(int32_t *tile_m, int32_t *tile_n) {
 
 const char *ftblas_last_error(void) { return ctx().err; }
 
+#ifdef FTB_WS_PROF
+// development builds only: per-CTA phase sums of gemm_ws_kernel (ftblas_ws.cuh), read and reset
+int ftblas_ws_prof_read(unsigned long long *out, int n) {
+    CK(cudaDeviceSynchronize(), "sync");
+    CK(cudaMemcpyFromSymbol(out, ws_prof, sizeof(unsigned long long) * (size_t)std::min(n, 1024 * 16)), "prof read");
+    static unsigned long long zero[1024 * 16];
+    CK(cudaMemcpyToSymbol(ws_prof, zero, sizeof(zero)), "prof reset");
+    return 0;
+}
+#endif
+
 int ftblas_release(void) {
     Ctx &c = ctx();
     cudaStreamSynchronize(c.stream);
-    c.ws.release(); c.ws_gen++; c.a_valid = false; c.rep.release(); c.plan_dev.release();
+    c.ws.release(); c.ws_gen++; c.a_valid = false; c.rep.release(); c.pend.release(); c.plan_dev.release();
     c.plan_uploaded = -1;
     c.hA.release(); c.hB.release(); c.hC.release();
     return 0;

@@ -117,6 +117,17 @@ struct Correction {  // == ftblas_correction (48 bytes)
 struct ReportHdr {  // device-side counters
     unsigned long long count, tiles_flagged, rows_flagged, cols_flagged;
 };
+// A correction candidate located by the persistent kernel's epilogue, recomputed after the
+// GEMM by correct_kernel (ftblas_ws.cuh): element (i, j) of the call's C, its stored value,
+// its C0, the row residual and whether it is a single-error location (kind 1).
+struct Pending {
+    long long i, j;
+    double cur, c0, residual;
+    int single, pad;
+};
+struct PendingHdr {
+    unsigned long long count;
+};
 
 struct GemmArgs {
     const double *A, *B;
@@ -151,6 +162,9 @@ struct GemmArgs {
     ReportHdr *rep;
     Correction *rep_entries;
     long long rep_cap;
+    PendingHdr *pend;        // correction candidates (persistent kernel, ftblas_ws.cuh)
+    Pending *pend_entries;
+    long long pend_cap;
     long long off_i, off_j;  // position of this call's C block in the caller's C (report indices)
     int vecC;              // C 16-byte aligned with even ldc (cp.async16 staging of C0)
 };
@@ -304,6 +318,7 @@ struct EncodeArgs {
     long long K, Kp, kper;
     int kch;
     ReportHdr *rep;  // zeroed here (stream-ordered before the GEMM kernel)
+    PendingHdr *pend;  // zeroed here on every FT call
     int op_base;     // operand of blockIdx.z = 0
 };
 
@@ -468,6 +483,7 @@ __global__ void __launch_bounds__(NTHREADS, 3) encode_kernel(EncodeArgs a) {
     if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0 && a.rep) {
         a.rep->count = 0; a.rep->tiles_flagged = 0; a.rep->rows_flagged = 0; a.rep->cols_flagged = 0;
     }
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0 && a.pend) a.pend->count = 0;
     if (t >= o.ntiles) return;
     const long long kbeg = (long long)ch * a.kper;
     const long long kend = min(kbeg + a.kper, a.Kp);
@@ -583,8 +599,16 @@ __device__ void warp_recompute(const GemmArgs &g, long long i, long long j, doub
     const int lane = threadIdx.x & 31;
     s = 0.0; sa = 0.0;
     for (long long k = lane; k < g.K; k += 32) {
+#if defined(FTB_DBG_NC)
+        const double a = __ldg(gaddr<KCA>(g.A, g.lda, i, k));
+        const double b = __ldg(gaddr<KCB>(g.B, g.ldb, j, k));
+#elif defined(FTB_DBG_CG)
+        const double a = __ldcg(gaddr<KCA>(g.A, g.lda, i, k));
+        const double b = __ldcg(gaddr<KCB>(g.B, g.ldb, j, k));
+#else
         const double a = *gaddr<KCA>(g.A, g.lda, i, k);
         const double b = *gaddr<KCB>(g.B, g.ldb, j, k);
+#endif
         s = fma(a, b, s);
         sa = fma(fabs(a), fabs(b), sa);
     }

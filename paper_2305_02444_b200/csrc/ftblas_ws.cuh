@@ -2,52 +2,112 @@
 //
 // One CTA per SM walks its share of the 128 x 128 tiles of C (tile x = blockIdx.x + i gridDim.x,
 // rasterized by tile_coords).  Three roles run concurrently:
-//   producer  (warp 12, one thread; all of warpgroup 3 for the cp.async fallback): streams the
-//             operand tiles of every k-tile of every tile of the CTA through a STAGES-deep TMA /
-//             mbarrier ring (the ring runs across tile boundaries) and prefetches each tile's C0
-//             into L2 near the end of its mainloop;
-//   MMA       (warps 0..7, 64 x 32 warp tiles, the mainloop of gemm_kernel<NWN = 4>): DMMA into
-//             registers; at the end of a tile the accumulators are injected with the planned
-//             flips (test harness), written to one of two TMEM buffers (tcgen05.st) and handed
-//             over with an mbarrier -- the warps start the next tile's mainloop at once;
+//   producer  (warp 12, one thread; all of warpgroup 3 for the non-TMA fallback): streams the
+//             operand tiles of every k-tile of every tile of the CTA through a WS_STAGES-deep
+//             TMA / mbarrier ring that runs across tile boundaries, and prefetches each tile's
+//             C0 into L2 near the end of its mainloop;
+//   MMA       (warps 0..7, 32 x 64 warp tiles: warp w owns rows 32 (w % 4) .. +31, columns
+//             64 (w / 4) .. +63): DMMA into registers; at the end of a tile the accumulators get
+//             the planned flips (test harness) and go to one of two TMEM buffers (tcgen05.st),
+//             handed over with an mbarrier -- the warps start the next tile's mainloop at once;
 //   epilogue  (warps 8..11): per tile, read the accumulators back from TMEM (tcgen05.ld), form
 //             out = alpha acc + beta C0 with the row / column sums of d = out - beta C0 and the
-//             |C0| maxima (reading R4k), verify every row and column against the checksum-GEMM
-//             references, locate and correct (lines 540, 521; readings
-//             R5-R7), and store the verified tile -- all while the MMA warps run the next tile.
-// TMEM is used as the accumulator hand-over buffer the DMMA path (FP64 tensor cores have no
-// tcgen05.mma kind) otherwise lacks: 2 buffers x 256 columns x 128 lanes x 32 bit = all 512
-// columns.  MMA warp w writes lanes 32 (w % 4) .. +31 (its TMEM sub-partition), columns
-// buf * 256 + (w / 4) * 128 + [0, 128): the 64 doubles of its accumulator in fragment order
-// (element (a, b, e) at words 16 a + 4 b + 2 e).  Epilogue warp ew (= warp % 4) reads the
-// same lanes, i.e. exactly the fragments of MMA warps ew and ew + 4 ("twins"), so the
-// epilogue reuses the fragment row / column maps of the mainloop.  DESIGN.md section 5.
+//             |C0| maxima (readings R3, R4k), verify every row and column against the checksum-
+//             GEMM references, locate and correct (lines 540, 521; readings
+//             R5-R7) and store the verified tile -- while the MMA warps run the next tile.
+// TMEM is the accumulator hand-over buffer the DMMA path (FP64 tensor cores have no tcgen05.mma
+// kind) otherwise lacks: 2 buffers x 256 columns x 128 lanes x 32 bit = all 512 columns, TMEM
+// lane = tile row.  MMA warp w stores with the 16x256b shape (a thread of fragment row g writes
+// lanes g and g + 8, the mma.sync accumulator layout), so fragments a = 2p, 2p + 1 land in lanes
+// 32 (w % 4) + 16 p + [0, 16) and a row's 64 doubles of warp column w / 4 fill TMEM columns
+// buf * 256 + (w / 4) * 128 + [0, 128).  Epilogue warp ew (= its TMEM sub-partition) therefore
+// owns rows 32 ew .. +31, one row per thread, and reads its row 8 columns at a time.
+// C0 comes in and the verified tile goes out through a 64 KB shared buffer (half a tile) with
+// TMA (bulk tensor load / store), so the epilogue issues no L1-allocating global loads: with
+// ~200 KB of shared memory in use, L1-allocating loads running beside the DMMA mainloop
+// corrupted accumulators ("L1-allocating loads beside the DMMA stream").
 #pragma once
 #include "ftblas_kernels.cuh"
 
 namespace ftb {
 
 constexpr int WS_THREADS = 512;                 // 8 MMA + 4 epilogue + 4 producer-group warps
-constexpr int WS_STAGES = 3;
+#ifndef FTB_WS_STAGES
+#define FTB_WS_STAGES 2
+#endif
+constexpr int WS_STAGES = FTB_WS_STAGES;
 constexpr int WS_STAGE_EL = 2 * TILE_EL;        // A 128 x BK | B 128 x BK
-constexpr int WS_SMEM = WS_STAGES * WS_STAGE_EL * 8 + 1024;
-// setmaxnreg split of the 64 K registers (one CTA per SM): the MMA warps hold 64 accumulators
-// + two sets of fragments; the non-FT epilogue needs fewer registers than the FT one
+constexpr int WS_CBUF_EL = 64 * BM;             // C staging: 64 columns x 128 rows (half a tile)
+constexpr int WS_SMEM = (WS_STAGES * WS_STAGE_EL + WS_CBUF_EL) * 8 + 1024;
+
+// setmaxnreg split of the 64 K registers (one CTA per SM)
 template <bool FT>
 struct WsRegs {
-    static constexpr int MMA = FT ? 184 : 192, EPI = FT ? 104 : 88, PROD = FT ? 40 : 32;
+    static constexpr int MMA = FT ? 184 : 200, EPI = FT ? 104 : 72, PROD = FT ? 40 : 32;
     static_assert(256 * MMA + 128 * EPI + 128 * PROD <= 65536,
                   "setmaxnreg budget exceeds the register file of one CTA per SM");
 };
-constexpr int WS_CAND = 256;                    // candidates per recompute batch (rare path)
 
-// ------------------------------------------------------------------ TMEM primitives
+// ------------------------------------------------------------------ phase timing (development)
+// -DFTB_WS_PROF: per-CTA globaltimer sums of the phases below (read by ftblas_ws_prof_read);
+// compiled out otherwise.
+#ifdef FTB_WS_PROF
+__device__ unsigned long long ws_prof[1024][16];
+__device__ __forceinline__ unsigned long long ws_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define WS_T(v) const unsigned long long v = ws_now()
+#define WS_ADD(slot, t0) ws_prof[blockIdx.x][slot] += ws_now() - (t0)
+#else
+#define WS_T(v)
+#define WS_ADD(slot, t0)
+#endif
+enum { WP_MMA_WAIT_FULL = 0, WP_MMA_WAIT_EMPTYACC, WP_MMA_TMEMST, WP_EPI_WAIT_ACC, WP_EPI_WAIT_C0, WP_EPI_PASS1,
+       WP_EPI_VERIFY, WP_EPI_PASS2, WP_EPI_STORE, WP_PROD_WAIT_EMPTY, WP_EPI_TOTAL, WP_MMA_TOTAL };
+
+// ------------------------------------------------------------------ primitives
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
-// 16 consecutive 32-bit TMEM columns of this thread's lane <- 8 doubles (lo, hi word pairs);
-// the store is waited for inside the same asm statement, so the source registers are free
-// afterwards whatever the compiler schedules next
+// read-only global data (operands, finalized side data, fault plan) without L1 allocation
+__device__ __forceinline__ double ld_ro(const double *p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ long long ld_ro(const long long *p) {
+    long long v;
+    asm volatile("ld.global.nc.L1::no_allocate.s64 %0, [%1];\n" : "=l"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int ld_ro(const int *p) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];\n" : "=r"(v) : "l"(p));
+    return v;
+}
+
+// Accumulator fragments a = 2p, 2p+1 (8 b x 2 e each) of an MMA thread -> TMEM lanes 16 p + g
+// and 16 p + 8 + g of its warp's sub-partition, 16x256b shape: repetition r = 2 b + e carries
+// {acc[2p][b][e], acc[2p+1][b][e]} into columns 8 r + 2 t of those two lanes.  8 repetitions per
+// instruction; the wait is inside the statement so the registers are free afterwards.
+__device__ __forceinline__ void tmem_st_pair8(unsigned taddr, const double *lo_row, const double *hi_row) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.16x256b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
+        "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};\n"
+        "tcgen05.wait::st.sync.aligned;\n" ::"r"(taddr),
+        "r"(__double2loint(lo_row[0])), "r"(__double2hiint(lo_row[0])), "r"(__double2loint(hi_row[0])), "r"(__double2hiint(hi_row[0])),
+        "r"(__double2loint(lo_row[1])), "r"(__double2hiint(lo_row[1])), "r"(__double2loint(hi_row[1])), "r"(__double2hiint(hi_row[1])),
+        "r"(__double2loint(lo_row[2])), "r"(__double2hiint(lo_row[2])), "r"(__double2loint(hi_row[2])), "r"(__double2hiint(hi_row[2])),
+        "r"(__double2loint(lo_row[3])), "r"(__double2hiint(lo_row[3])), "r"(__double2loint(hi_row[3])), "r"(__double2hiint(hi_row[3])),
+        "r"(__double2loint(lo_row[4])), "r"(__double2hiint(lo_row[4])), "r"(__double2loint(hi_row[4])), "r"(__double2hiint(hi_row[4])),
+        "r"(__double2loint(lo_row[5])), "r"(__double2hiint(lo_row[5])), "r"(__double2loint(hi_row[5])), "r"(__double2hiint(hi_row[5])),
+        "r"(__double2loint(lo_row[6])), "r"(__double2hiint(lo_row[6])), "r"(__double2loint(hi_row[6])), "r"(__double2hiint(hi_row[6])),
+        "r"(__double2loint(lo_row[7])), "r"(__double2hiint(lo_row[7])), "r"(__double2loint(hi_row[7])), "r"(__double2hiint(hi_row[7]))
+        : "memory");
+}
+// 8 doubles of this thread's TMEM lane <-> 16 consecutive columns (32x32b shape)
 __device__ __forceinline__ void tmem_st8d(unsigned taddr, const double *v) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};\n"
@@ -58,8 +118,6 @@ __device__ __forceinline__ void tmem_st8d(unsigned taddr, const double *v) {
         "r"(__double2loint(v[6])), "r"(__double2hiint(v[6])), "r"(__double2loint(v[7])), "r"(__double2hiint(v[7]))
         : "memory");
 }
-// 8 doubles <- 16 consecutive TMEM columns (load and wait in one statement: the registers
-// are valid when it returns)
 __device__ __forceinline__ void tmem_ld8d(unsigned taddr, double *v) {
     int w[16];
     asm volatile(
@@ -73,27 +131,66 @@ __device__ __forceinline__ void tmem_ld8d(unsigned taddr, double *v) {
     for (int q = 0; q < 8; q++) v[q] = __hiloint2double(w[2 * q + 1], w[2 * q]);
 }
 
-// verification tile references of tile (tm, tn) -> smem (FT): finalized norms and checksum-GEMM
-// slices (side_finalize_kernel / single-split R, S read in place), one row and one column per
-// epilogue thread
+// TMA of the C staging buffer: box {128 rows, 64 columns} of C (column-major, dense in smem)
+__device__ __forceinline__ void tma_load_c(double *dst, const CUtensorMap *map, unsigned long long *bar, int row0,
+                                           int col0) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::
+            "r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(row0), "r"(col0)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_c(const CUtensorMap *map, const double *src, int row0, int col0) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];\n" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(row0), "r"(col0)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// Non-TMA operand staging (pointer not 16-byte aligned or odd ld): the producer group copies
+// the tile element by element through registers, read-only loads that bypass L1 (see above),
+// zero-fill outside [0, MNd) x [0, Kd); the caller arrives on the stage barrier afterwards.
+template <bool KC, int ROWS, int NTP>
+__device__ __forceinline__ void produce_tile_ro(double *s, const double *X, long long ld, long long mn0, long long k0,
+                                                long long MNd, long long Kd, int pt) {
+#pragma unroll 4
+    for (int c = pt; c < ROWS * BK; c += NTP) {
+        int mn, k;
+        if (KC) { mn = c / BK; k = c % BK; }
+        else    { k = c / ROWS; mn = c % ROWS; }
+        const long long gmn = mn0 + mn, gk = k0 + k;
+        s[Tile<KC, ROWS>::idx(mn, k)] = (gmn < MNd && gk < Kd) ? ld_ro(gaddr<KC>(X, ld, gmn, gk)) : 0.0;
+    }
+}
+
+template <int V>
+struct IntC {
+    static constexpr int value = V;
+};
+
+// verification references of one tile (FT): finalized norms and checksum-GEMM slices
 struct WsSide {
     double nrm_row[BM], nrm_col[BN], pre_r[BM], pre_s[BN], nrm_max[2];
 };
 
+// GemmArgs.vecC != 0 and a tensor map for C (tmC) <=> C0 / C move by TMA; else the epilogue
+// copies the staging buffer with L2-only loads and plain stores.
 template <bool KCA, bool KCB, bool TMA, bool FT>
 __global__ void __launch_bounds__(WS_THREADS, 1)
     gemm_ws_kernel(const __grid_constant__ GemmArgs g, const __grid_constant__ CUtensorMap tmA,
-                   const __grid_constant__ CUtensorMap tmB) {
+                   const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmC) {
     extern __shared__ __align__(1024) double smem_raw[];
-    __shared__ __align__(8) unsigned long long full_bar[WS_STAGES], empty_bar[WS_STAGES], acc_full[2], acc_empty[2];
+    __shared__ __align__(8) unsigned long long full_bar[WS_STAGES], empty_bar[WS_STAGES], acc_full[2], acc_empty[2],
+        c0_bar;
     __shared__ unsigned tmem_base_sh;
     __shared__ WsSide side;
-    __shared__ double red_r[4][BM], red_c[2][BN], dres[BM];  // row partials per warp column
-    __shared__ unsigned redm_r[4][BM], redm_c[2][BN];
+    __shared__ double red_c[4][BN], dres[BM];  // column partials per epilogue warp (32 rows each)
+    __shared__ unsigned redm_c[4][BN];
     __shared__ int flags[2 + BM + BN];
-    __shared__ int rrank[BM], crank[BN];
-    __shared__ double cand_y[FT ? WS_CAND : 1], cand_eb[FT ? WS_CAND : 1];
+    __shared__ int rflag[BM], cflag[BN];
     double *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) / 8u;
+    double *cbuf = smem + WS_STAGES * WS_STAGE_EL;  // [64 columns][128 rows]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long ntm = (g.M + BM - 1) / BM, ntn = (g.N + BN - 1) / BN, ntiles = ntm * ntn;
     const int ktiles = (g.alpha == 0.0) ? 0 : (int)((g.K + BK - 1) / BK);
@@ -101,13 +198,14 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
 
     if (tid == 0) {
         for (int s = 0; s < WS_STAGES; s++) {
-            mbar_init(&full_bar[s], 1 + (TMA ? 0 : PT));
+            mbar_init(&full_bar[s], TMA ? 1 : PT);
             mbar_init(&empty_bar[s], 8);     // one arrival per MMA warp
         }
         for (int b = 0; b < 2; b++) {
             mbar_init(&acc_full[b], 8);      // MMA warps: accumulators in TMEM
             mbar_init(&acc_empty[b], 4);     // epilogue warps: buffer read
         }
+        mbar_init(&c0_bar, 1);               // C0 half-tile TMA (expect_tx by the issuing thread)
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == 13) {  // TMEM: all 512 columns (two accumulator buffers); one CTA per SM
@@ -125,24 +223,33 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(WsRegs<FT>::PROD));
         const int pt = tid - 384;
         if (TMA ? pt == 0 : true) {
-            constexpr unsigned TX = TMA ? 2u * TILE_EL * 8u : 0u;
+            constexpr unsigned TX = 2u * TILE_EL * 8u;
             unsigned kg = 0;
             for (long long x = blockIdx.x; x < ntiles; x += gridDim.x) {
                 long long tm, tn;
                 tile_coords(x, ntm, ntn, tm, tn);
                 const long long m0 = tm * BM, n0 = tn * BN;
-                const int pf_kt = max(0, ktiles - WS_STAGES - 1);
+                const int pf_kt = max(0, ktiles - WS_STAGES - 2);
                 for (int kt = 0; kt < ktiles; kt++, kg++) {
                     const int st = (int)(kg % WS_STAGES);
-                    if (kg >= WS_STAGES) mbar_wait(&empty_bar[st], ((kg / WS_STAGES) - 1) & 1);
+                    if (kg >= WS_STAGES) {
+                        WS_T(t0);
+                        mbar_wait(&empty_bar[st], ((kg / WS_STAGES) - 1) & 1);
+                        if (pt == 0) WS_ADD(WP_PROD_WAIT_EMPTY, t0);
+                    }
                     double *sa = smem + st * WS_STAGE_EL;
-                    if (pt == 0) mbar_arrive_expect_tx(&full_bar[st], TX);
-                    produce_tile<KCA, TMA, 128, PT>(sa, &tmA, &full_bar[st], g.A, g.lda, m0, (long long)kt * BK, g.M, g.K, pt);
-                    produce_tile<KCB, TMA, 128, PT>(sa + TILE_EL, &tmB, &full_bar[st], g.B, g.ldb, n0, (long long)kt * BK,
-                                                    g.N, g.K, pt);
-                    if (!TMA) cp_async_mbar_arrive(&full_bar[st]);
+                    const long long k0 = (long long)kt * BK;
+                    if (TMA) {
+                        mbar_arrive_expect_tx(&full_bar[st], TX);
+                        produce_tile<KCA, true, 128, PT>(sa, &tmA, &full_bar[st], g.A, g.lda, m0, k0, g.M, g.K, 0);
+                        produce_tile<KCB, true, 128, PT>(sa + TILE_EL, &tmB, &full_bar[st], g.B, g.ldb, n0, k0, g.N, g.K, 0);
+                    } else {
+                        produce_tile_ro<KCA, 128, PT>(sa, g.A, g.lda, m0, k0, g.M, g.K, pt);
+                        produce_tile_ro<KCB, 128, PT>(sa + TILE_EL, g.B, g.ldb, n0, k0, g.N, g.K, pt);
+                        mbar_arrive(&full_bar[st]);  // release: this thread's smem writes
+                    }
                     if (pt == 0 && kt == pf_kt && g.beta != 0.0 && g.vecC) {
-                        // C0 of this tile -> L2 shortly before its epilogue reads it
+                        // C0 of this tile -> L2 shortly before its epilogue loads it
                         const unsigned bytes = (unsigned)(min((long long)BM, g.M - m0) * 8) & ~15u;
                         const long long nv = min((long long)BN, g.N - n0);
                         if (bytes)
@@ -150,147 +257,226 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                     }
                 }
             }
-            if (!TMA) cp_wait<0>();
         }
     } else if (warp >= 8) {
         // ------------------------------------------------------------------ epilogue
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(WsRegs<FT>::EPI));
         const int ew = warp - 8, et = tid - 256;  // epilogue warp (= TMEM sub-partition), thread
-        const int wm = ew & 1, wn0 = ew >> 1;     // twins: MMA warps ew (wn0) and ew + 4 (wn0 + 2)
         auto epi_bar = [&]() { asm volatile("bar.sync 2, 128;\n" ::: "memory"); };
-        const bool beta0 = g.beta == 0.0, beta1 = g.beta == 1.0;
+        // beta classes decided once on the integer pipe (FP64 instructions beside the DMMA stream
+        // wait for the tensor pipe: every one in the per-element code costs)
+        const long long bbits = __double_as_longlong(g.beta);
+        const bool beta0 = (bbits << 1) == 0, beta1 = bbits == 0x3ff0000000000000ll;
+        const int bmode = beta0 ? 0 : (beta1 ? 1 : 2);
         const double aa = fabs(g.alpha), ab = fabs(g.beta);
-        auto row_of = [&](int a) { return frag_mn<KCA>(wm * 64, a, lane >> 2); };
-        auto col_of = [&](int t, int b, int e) { return frag_mn<KCB>((wn0 + 2 * t) * 32, b, 2 * (lane & 3) + e); };
+        // this thread's row of every tile (TMEM lane 32 ew + lane) and the columns of the 8
+        // doubles of TMEM chunk j of warp column wn (q = 4 e + t)
+        const int row = frag_mn<KCA>(32 * ew, lane >> 3, lane & 7);
+        auto col_of = [&](int wn, int j, int q) { return frag_mn<KCB>(64 * wn, j, 2 * (q & 3) + (q >> 2)); };
+        const bool tma_c = g.vecC != 0;
+        const bool need_c0 = !beta0;
+        unsigned c0_phase = 0;
+        // C0 half h of the tile at (m0, n0) -> cbuf: TMA by thread 0, or L2-only loads by all
+        auto load_c0 = [&](long long m0, long long n0, int h) {
+            if (tma_c) {
+                if (et == 0) {
+                    mbar_arrive_expect_tx(&c0_bar, (unsigned)(WS_CBUF_EL * 8));
+                    tma_load_c(cbuf, &tmC, &c0_bar, (int)m0, (int)(n0 + 64 * h));
+                }
+            } else {
+                const long long gi = m0 + et;
+                for (int c = 0; c < 64; c++) {
+                    const long long gj = n0 + 64 * h + c;
+                    cbuf[c * BM + et] = (gi < g.M && gj < g.N) ? __ldcg(g.C + gi + gj * g.ldc) : 0.0;
+                }
+            }
+        };
+        auto wait_c0 = [&]() {
+            if (tma_c) {
+                mbar_wait(&c0_bar, c0_phase);
+                c0_phase ^= 1u;
+            } else {
+                epi_bar();
+            }
+        };
+        // cbuf (half h) -> C of the tile at (m0, n0); the buffer is reusable when this returns
+        auto store_c = [&](long long m0, long long n0, int h, long long mvalid, long long nvalid) {
+            if (tma_c) {
+                fence_proxy_async_smem();  // generic-proxy writes of cbuf -> visible to the TMA
+                epi_bar();
+                if (et == 0) {
+                    tma_store_c(&tmC, cbuf, (int)m0, (int)(n0 + 64 * h));
+                    tma_store_wait_read();
+                }
+                epi_bar();
+            } else {
+                epi_bar();
+                if (et < mvalid)
+                    for (int c = 0; c < 64 && 64 * h + c < nvalid; c++)
+                        g.C[(m0 + et) + (n0 + 64 * h + c) * g.ldc] = cbuf[c * BM + et];
+                epi_bar();
+            }
+        };
         int it = 0;
+        if (blockIdx.x < ntiles && need_c0) {
+            long long tm, tn;
+            tile_coords(blockIdx.x, ntm, ntn, tm, tn);
+            load_c0(tm * BM, tn * BN, 0);
+        }
         for (long long x = blockIdx.x; x < ntiles; x += gridDim.x, it++) {
             long long tm, tn;
             tile_coords(x, ntm, ntn, tm, tn);
             const long long m0 = tm * BM, n0 = tn * BN;
             const long long mvalid = min((long long)BM, g.M - m0), nvalid = min((long long)BN, g.N - n0);
+            const bool rowok = row < mvalid;
             if (FT) {  // side data of this tile (loads overlap the wait for the accumulators)
                 const long long gi = m0 + et, gj = n0 + et;
-                side.nrm_row[et] = et < mvalid ? g.fin_nrmA[gi] : 0.0;
-                side.pre_r[et] = et < mvalid ? g.fin_R[tn * g.M + gi] : 0.0;
-                side.nrm_col[et] = et < nvalid ? g.fin_nrmB[gj] : 0.0;
-                side.pre_s[et] = et < nvalid ? g.fin_S[tm * g.N + gj] : 0.0;
+                side.nrm_row[et] = et < mvalid ? ld_ro(g.fin_nrmA + gi) : 0.0;
+                side.pre_r[et] = et < mvalid ? ld_ro(g.fin_R + tn * g.M + gi) : 0.0;
+                side.nrm_col[et] = et < nvalid ? ld_ro(g.fin_nrmB + gj) : 0.0;
+                side.pre_s[et] = et < nvalid ? ld_ro(g.fin_S + tm * g.N + gj) : 0.0;
                 if (et == 0) {
-                    side.nrm_max[0] = g.fin_maxA[tm];
-                    side.nrm_max[1] = g.fin_maxB[tn];
+                    side.nrm_max[0] = ld_ro(g.fin_maxA + tm);
+                    side.nrm_max[1] = ld_ro(g.fin_maxB + tn);
                     flags[0] = 0;
                     flags[1] = 0;
                 }
             }
             const int buf = it & 1;
+            WS_T(tw0);
             mbar_wait(&acc_full[buf], (unsigned)((it >> 1) & 1));
+            if (et == 0) WS_ADD(WP_EPI_WAIT_ACC, tw0);
+            WS_T(tp1);
             tc_fence_after();
             const unsigned tb = tbase + ((unsigned)(32 * ew) << 16) + (unsigned)(buf * 256);
-            // ---- pass 1: out, sums, maxima (FT: out back into TMEM in place; non-FT: stored).
-            // Twin t (MMA warp ew + 4 t, warp column wn0 + 2 t) row by row: the row partial of a
-            // fragment row over this twin's 32 columns (8 elements per lane, 4 lanes per row), the
-            // column partials over this warp's 64 rows carried across the rows.
-#pragma unroll 1
-            for (int t = 0; t < 2; t++) {
-                double cs[8];
+            // ---- pass 1, half h = warp column wn: out, the row sum, column partials.  One chunk =
+            // 8 doubles of this thread's row; the row sum keeps 8 independent partials (one per
+            // chunk position q, combined in fixed order after the tile) so the FP64 adds do not
+            // form one 128-long dependency chain.
+            double rsq[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) rsq[q] = 0.0;
+            unsigned rm = 0u;
+            auto chunk = [&](auto mode_c, int h, int j) {
+                constexpr int MODE = decltype(mode_c)::value;  // 0: beta = 0, 1: beta = 1, 2: other
+                double v[8], cs[8];
                 unsigned cm[8];
+                tmem_ld8d(tb + h * 128 + 16 * j, v);
 #pragma unroll
-                for (int q = 0; q < 8; q++) { cs[q] = 0.0; cm[q] = 0u; }
-#pragma unroll 1
-                for (int a = 0; a < 8; a++) {
-                    double v[8];
-                    tmem_ld8d(tb + t * 128 + 16 * a, v);
-                    const int row = row_of(a);
-                    const long long gi = m0 + row;
-                    double rsa = 0.0;
-                    unsigned rma = 0u;
-#pragma unroll
-                    for (int q = 0; q < 8; q++) {
-                        const int col = col_of(t, q >> 1, q & 1);
-                        const bool ok = row < mvalid && col < nvalid;
-                        const long long off = gi + (n0 + col) * g.ldc;
-                        double o, d;
-                        if (beta0) {
-                            o = g.alpha * v[q];
-                            d = o;
-                        } else {
-                            const double c0 = ok ? g.C[off] : 0.0;
-                            const double tt = beta1 ? c0 : g.beta * c0;
-                            o = fma(g.alpha, v[q], tt);
-                            d = o - tt;
-                            if (FT) {
-                                const unsigned h = (unsigned)__double2hiint(c0) & 0x7fffffffu;
-                                rma = max(rma, h);
-                                cm[q] = max(cm[q], h);
-                            }
-                        }
+                for (int q = 0; q < 8; q++) {
+                    const int col = col_of(h, j, q);          // column in the tile
+                    const int cl = col - 64 * h;               // column in the half
+                    double o, d;
+                    cm[q] = 0u;
+                    if (MODE == 0) {
+                        o = g.alpha * v[q];
+                        d = o;
+                    } else {
+                        const double c0 = cbuf[cl * BM + row];  // 0 outside M x N (TMA zero fill)
+                        const double tt = MODE == 1 ? c0 : g.beta * c0;
+                        o = fma(g.alpha, v[q], tt);
+                        d = o - tt;
                         if (FT) {
-                            d = ok ? d : 0.0;
-                            rsa += d;
-                            cs[q] += d;
-                            v[q] = o;
-                        } else if (ok) {
-                            g.C[off] = o;
+                            const unsigned hw = (unsigned)__double2hiint(c0) & 0x7fffffffu;
+                            rm = max(rm, hw);
+                            cm[q] = hw;
                         }
                     }
                     if (FT) {
-                        tmem_st8d(tb + t * 128 + 16 * a, v);
-                        // the row's 4 lanes (lane bits 0, 1)
-                        rsa += __shfl_xor_sync(0xffffffffu, rsa, 1);
-                        rsa += __shfl_xor_sync(0xffffffffu, rsa, 2);
-                        rma = max(rma, __shfl_xor_sync(0xffffffffu, rma, 1));
-                        rma = max(rma, __shfl_xor_sync(0xffffffffu, rma, 2));
-                        if ((lane & 3) == 0) {
-                            red_r[wn0 + 2 * t][row] = rsa;
-                            redm_r[wn0 + 2 * t][row] = rma;
-                        }
+                        d = (rowok && col < nvalid) ? d : 0.0;
+                        rsq[q] += d;
+                        cs[q] = d;
+                        v[q] = o;
+                    } else {
+                        cbuf[cl * BM + row] = o;
                     }
                 }
                 if (FT) {
-                    // column sums over this warp's 64 rows: 8 (b, e) values per lane over the 8
-                    // lanes of a column (lane bits 2..4), transposing butterfly -> one column per lane
+                    tmem_st8d(tb + h * 128 + 16 * j, v);
+                    // column sums over this warp's 32 rows: transposing butterfly over lane bits
+                    // 4, 3, 2 (8 -> 1 value per lane), then plain over bits 1, 0
 #pragma unroll
-                    for (int off = 4; off <= 16; off <<= 1) {
+                    for (int off = 16; off >= 4; off >>= 1) {
                         const bool up = (lane & off) != 0;
-                        const int h = 8 * 4 / (2 * off);  // 4, 2, 1 values kept
+                        const int hh = off / 4;  // 4, 2, 1 values kept
 #pragma unroll
-                        for (int j = 0; j < 4; j++) {
-                            if (j < h) {
-                                const double send = up ? cs[j] : cs[j + h];
-                                const double keep = up ? cs[j + h] : cs[j];
-                                cs[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-                                const unsigned msend = up ? cm[j] : cm[j + h];
-                                const unsigned mkeep = up ? cm[j + h] : cm[j];
-                                cm[j] = max(mkeep, __shfl_xor_sync(0xffffffffu, msend, off));
+                        for (int i2 = 0; i2 < 4; i2++) {
+                            if (i2 < hh) {
+                                const double send = up ? cs[i2] : cs[i2 + hh];
+                                const double keep = up ? cs[i2 + hh] : cs[i2];
+                                cs[i2] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                                if (MODE != 0) {
+                                    const unsigned ms = up ? cm[i2] : cm[i2 + hh];
+                                    const unsigned mk = up ? cm[i2 + hh] : cm[i2];
+                                    cm[i2] = max(mk, __shfl_xor_sync(0xffffffffu, ms, off));
+                                }
                             }
                         }
                     }
-                    const int q = ((lane >> 2) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 4) & 1);
-                    const int col = col_of(t, q >> 1, q & 1);
-                    red_c[wm][col] = cs[0];
-                    redm_c[wm][col] = cm[0];
+                    cs[0] += __shfl_xor_sync(0xffffffffu, cs[0], 2);
+                    cs[0] += __shfl_xor_sync(0xffffffffu, cs[0], 1);
+                    if (MODE != 0) {
+                        cm[0] = max(cm[0], __shfl_xor_sync(0xffffffffu, cm[0], 2));
+                        cm[0] = max(cm[0], __shfl_xor_sync(0xffffffffu, cm[0], 1));
+                    }
+                    if ((lane & 3) == 0) {
+                        const int q = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+                        const int col = col_of(h, j, q);
+                        red_c[ew][col] = cs[0];
+                        redm_c[ew][col] = cm[0];
+                    }
+                }
+            };
+#pragma unroll 1
+            for (int h = 0; h < 2; h++) {
+                if (need_c0) {
+                    WS_T(tc0);
+                    wait_c0();
+                    if (et == 0) WS_ADD(WP_EPI_WAIT_C0, tc0);
+                }
+                if (bmode == 0) {
+#pragma unroll 1
+                    for (int j = 0; j < 8; j++) chunk(IntC<0>{}, h, j);
+                } else if (bmode == 1) {
+#pragma unroll 1
+                    for (int j = 0; j < 8; j++) chunk(IntC<1>{}, h, j);
+                } else {
+#pragma unroll 1
+                    for (int j = 0; j < 8; j++) chunk(IntC<2>{}, h, j);
+                }
+                if (!FT) {
+                    WS_T(ts0);
+                    store_c(m0, n0, h, mvalid, nvalid);
+                    if (et == 0) WS_ADD(WP_EPI_STORE, ts0);
+                    if (h == 0 && need_c0) load_c0(m0, n0, 1);
+                } else if (h == 0 && need_c0) {
+                    epi_bar();  // every thread done reading C0 half 0
+                    load_c0(m0, n0, 1);
                 }
             }
+            if (et == 0) WS_ADD(WP_EPI_PASS1, tp1);
+            WS_T(tv0);
             if (FT) {
                 epi_bar();
-                // ---- verification (readings R3, R4, R4k): thread et checks
-                // row et and column et
-                auto c0_bound = [&](unsigned h, long long n) {
-                    if (h >= 0x7ff00000u) return __longlong_as_double(0x7ff0000000000000ll);
-                    return (double)n * __hiloint2double((int)(h + 1u), 0);
+                // ---- verification (readings R3, R4, R4k): each thread checks
+                // its own row (the whole row sum is in-thread) and column et
+                auto c0_bound = [&](unsigned hw, long long n) {
+                    if (hw >= 0x7ff00000u) return __longlong_as_double(0x7ff0000000000000ll);
+                    return (double)n * __hiloint2double((int)(hw + 1u), 0);
                 };
-                if (et < mvalid) {
-                    const double sum = (red_r[0][et] + red_r[1][et]) + (red_r[2][et] + red_r[3][et]);
-                    const double c0a = beta0 ? 0.0 : c0_bound(max(max(redm_r[0][et], redm_r[1][et]),
-                                                                  max(redm_r[2][et], redm_r[3][et])), nvalid);
+                if (rowok) {
+                    const double rs = ((rsq[0] + rsq[1]) + (rsq[2] + rsq[3])) + ((rsq[4] + rsq[5]) + (rsq[6] + rsq[7]));
+                    const double c0a = beta0 ? 0.0 : c0_bound(rm, nvalid);
                     const double tau = 4.0 * U_ROUND * (double)(g.K + nvalid + 3) *
-                                       (aa * side.nrm_row[et] * side.nrm_max[1] + ab * c0a);
-                    const double d = sum - g.alpha * side.pre_r[et];
-                    dres[et] = d;
-                    if (!(fabs(d) <= tau)) flags[2 + atomicAdd(&flags[0], 1)] = et;
+                                       (aa * side.nrm_row[row] * side.nrm_max[1] + ab * c0a);
+                    const double d = rs - g.alpha * side.pre_r[row];
+                    dres[row] = d;
+                    if (!(fabs(d) <= tau)) flags[2 + atomicAdd(&flags[0], 1)] = row;
                 }
                 if (et < nvalid) {
-                    const double sum = red_c[0][et] + red_c[1][et];
-                    const double c0a = beta0 ? 0.0 : c0_bound(max(redm_c[0][et], redm_c[1][et]), mvalid);
+                    const double sum = (red_c[0][et] + red_c[1][et]) + (red_c[2][et] + red_c[3][et]);
+                    const unsigned mx = max(max(redm_c[0][et], redm_c[1][et]), max(redm_c[2][et], redm_c[3][et]));
+                    const double c0a = beta0 ? 0.0 : c0_bound(mx, mvalid);
                     const double tau = 4.0 * U_ROUND * (double)(g.K + mvalid + 3) *
                                        (aa * side.nrm_max[0] * side.nrm_col[et] + ab * c0a);
                     const double d = sum - g.alpha * side.pre_s[et];
@@ -299,118 +485,94 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 epi_bar();
                 const int nr = flags[0], nc = flags[1];
                 if (nr != 0 || nc != 0) {
-                    // ---- locate + correct (rare): candidates = (flagged rows, or all rows) x
-                    // (flagged columns, or all columns) (readings R5, R7), recomputed from the
-                    // definition by the 4 epilogue warps (reading R6), decided by the owner of
-                    // the element in TMEM
+                    // ---- locate (rare): candidates = (flagged rows, or all rows) x (flagged
+                    // columns, or all columns) (readings R5, R7).  Each row owner lists its
+                    // candidates with their stored value and C0 (C is not yet overwritten); the
+                    // K-long recomputation and the correction (reading R6) run after the GEMM in
+                    // correct_kernel, so no long phase runs beside the DMMA mainloop.
                     if (et == 0) {
                         atomicAdd(&g.rep->tiles_flagged, 1ull);
                         atomicAdd(&g.rep->rows_flagged, (unsigned long long)nr);
                         atomicAdd(&g.rep->cols_flagged, (unsigned long long)nc);
-                        for (int x1 = 1; x1 < nr; x1++)
-                            for (int y = x1; y > 0 && flags[2 + y - 1] > flags[2 + y]; y--) {
-                                const int tt = flags[2 + y]; flags[2 + y] = flags[2 + y - 1]; flags[2 + y - 1] = tt;
-                            }
-                        for (int x1 = 1; x1 < nc; x1++)
-                            for (int y = x1; y > 0 && flags[2 + BM + y - 1] > flags[2 + BM + y]; y--) {
-                                const int tt = flags[2 + BM + y];
-                                flags[2 + BM + y] = flags[2 + BM + y - 1];
-                                flags[2 + BM + y - 1] = tt;
-                            }
                     }
-                    rrank[et] = (nr == 0 && et < mvalid) ? et : -1;
-                    crank[et] = (nc == 0 && et < nvalid) ? et : -1;
+                    rflag[et] = (nr == 0 && et < mvalid) ? 1 : 0;
+                    cflag[et] = (nc == 0 && et < nvalid) ? 1 : 0;
                     epi_bar();
-                    if (et < nr) rrank[flags[2 + et]] = et;
-                    if (et < nc) crank[flags[2 + BM + et]] = et;
+                    if (et < nr) rflag[flags[2 + et]] = 1;
+                    if (et < nc) cflag[flags[2 + BM + et]] = 1;
                     epi_bar();
                     const bool single = nr == 1 && nc == 1;  // Huang-Abraham location (line 540)
-                    const long long ncr = nr ? nr : mvalid, ncc = nc ? nc : nvalid, ncand = ncr * ncc;
-                    for (long long base = 0; base < ncand; base += WS_CAND) {
-                        const long long nb = min((long long)WS_CAND, ncand - base);
-                        for (long long q = ew; q < nb; q += 4) {
-                            const long long idx = base + q;
-                            const int rr = (int)(idx % ncr), cc = (int)(idx / ncr);
-                            const int r = nr ? flags[2 + rr] : rr, c = nc ? flags[2 + BM + cc] : cc;
-                            const long long gi = m0 + r, gj = n0 + c;
-                            double s, sa;
-                            warp_recompute<KCA, KCB>(g, gi, gj, s, sa);
-                            if (lane == 0) {
-                                const double c0 = beta0 ? 0.0 : g.C[gi + gj * g.ldc];  // C not yet stored
-                                cand_y[q] = beta0 ? g.alpha * s : fma(g.alpha, s, g.beta * c0);
-                                cand_eb[q] = 4.0 * U_ROUND * (double)(g.K + 3) * (aa * sa + ab * fabs(c0));
-                            }
-                        }
-                        epi_bar();
+                    const bool mine = rflag[row] != 0;
+                    if (__any_sync(0xffffffffu, mine)) {
 #pragma unroll 1
-                        for (int t = 0; t < 2; t++)
+                        for (int h = 0; h < 2; h++)
 #pragma unroll 1
-                            for (int a = 0; a < 8; a++) {
+                            for (int j = 0; j < 8; j++) {
                                 double v[8];
-                                tmem_ld8d(tb + t * 128 + 16 * a, v);
-                                const int row = row_of(a), rr = rrank[row];
-                                bool changed = false;
+                                tmem_ld8d(tb + h * 128 + 16 * j, v);
 #pragma unroll
                                 for (int q = 0; q < 8; q++) {
-                                    const int col = col_of(t, q >> 1, q & 1), cc = crank[col];
-                                    if (rr < 0 || cc < 0) continue;
-                                    const long long idx = (long long)cc * ncr + rr - base;
-                                    if (idx < 0 || idx >= nb) continue;
-                                    const double y = cand_y[idx];
-                                    if (single || !(fabs(v[q] - y) <= cand_eb[idx])) {
-                                        v[q] = y;  // correction (reading R6: the recomputed element)
-                                        changed = true;
-                                        const unsigned long long p = atomicAdd(&g.rep->count, 1ull);
-                                        if ((long long)p < g.rep_cap) {
-                                            Correction cr;
-                                            cr.tile_m = tm + g.off_i / BM; cr.tile_n = tn + g.off_j / BN;
-                                            cr.i = m0 + row + g.off_i; cr.j = n0 + col + g.off_j;
-                                            cr.residual = dres[row];
-                                            cr.kind = single ? 1 : 2; cr.pad = 0;
-                                            g.rep_entries[p] = cr;
-                                        }
+                                    const int col = col_of(h, j, q);
+                                    if (!mine || !cflag[col]) continue;
+                                    const unsigned long long p = atomicAdd(&g.pend->count, 1ull);
+                                    if ((long long)p < g.pend_cap) {
+                                        Pending pe;
+                                        pe.i = m0 + row; pe.j = n0 + col;
+                                        pe.cur = v[q];
+                                        pe.c0 = beta0 ? 0.0 : __ldcg(g.C + (m0 + row) + (n0 + col) * g.ldc);
+                                        pe.residual = dres[row];
+                                        pe.single = single ? 1 : 0; pe.pad = 0;
+                                        g.pend_entries[p] = pe;
                                     }
                                 }
-                                if (__any_sync(0xffffffffu, changed)) tmem_st8d(tb + t * 128 + 16 * a, v);
                             }
-                        epi_bar();
                     }
                 }
-                // ---- pass 2: store the verified tile
+                if (et == 0) WS_ADD(WP_EPI_VERIFY, tv0);
+                WS_T(tq0);
+                // ---- pass 2: the verified tile -> cbuf -> C, half by half
 #pragma unroll 1
-                for (int t = 0; t < 2; t++)
-#pragma unroll 2
-                    for (int a = 0; a < 8; a++) {
+                for (int h = 0; h < 2; h++) {
+#pragma unroll 1
+                    for (int j = 0; j < 8; j++) {
                         double v[8];
-                        tmem_ld8d(tb + t * 128 + 16 * a, v);
-                        const int row = row_of(a);
+                        tmem_ld8d(tb + h * 128 + 16 * j, v);
 #pragma unroll
-                        for (int q = 0; q < 8; q++) {
-                            const int col = col_of(t, q >> 1, q & 1);
-                            if (row < mvalid && col < nvalid) g.C[(m0 + row) + (n0 + col) * g.ldc] = v[q];
-                        }
+                        for (int q = 0; q < 8; q++) cbuf[(col_of(h, j, q) - 64 * h) * BM + row] = v[q];
                     }
+                    WS_T(ts1);
+                    store_c(m0, n0, h, mvalid, nvalid);
+                    if (et == 0) WS_ADD(WP_EPI_STORE, ts1);
+                }
+                if (et == 0) WS_ADD(WP_EPI_PASS2, tq0);
             }
-            // buffer read: hand it back to the MMA warps
+            // accumulator buffer read: hand it back to the MMA warps; C0 of the next tile
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[buf]);
+            if (need_c0 && x + gridDim.x < ntiles) {
+                long long tm2, tn2;
+                tile_coords(x + gridDim.x, ntm, ntn, tm2, tn2);
+                load_c0(tm2 * BM, tn2 * BN, 0);
+            }
             epi_bar();  // side data / flags / reductions of this tile consumed by every thread
+            if (et == 0) WS_ADD(WP_EPI_TOTAL, tw0);
         }
+        if (tma_c && et == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // stores done
     } else {
         // ------------------------------------------------------------------ MMA warps
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(WsRegs<FT>::MMA));
-        const int wm = warp % 2, wn = warp / 2;
-        const FragAddr<KCA> fA(wm * 64, lane);
-        const FragAddr<KCB> fB(wn * 32, lane);
-        auto row_of = [&](int a) { return frag_mn<KCA>(wm * 64, a, lane >> 2); };
-        auto col_of = [&](int b, int e) { return frag_mn<KCB>(wn * 32, b, 2 * (lane & 3) + e); };
-        double acc[8][4][2];
+        const int wm = warp & 3, wn = warp >> 2;  // rows 32 wm, columns 64 wn of the tile
+        const FragAddr<KCA> fA(wm * 32, lane);
+        const FragAddr<KCB> fB(wn * 64, lane);
+        auto row_of = [&](int a) { return frag_mn<KCA>(wm * 32, a, lane >> 2); };
+        auto col_of = [&](int b, int e) { return frag_mn<KCB>(wn * 64, b, 2 * (lane & 3) + e); };
+        double acc[4][8][2];
         auto zero_acc = [&]() {
 #pragma unroll
-            for (int a = 0; a < 8; a++)
+            for (int a = 0; a < 4; a++)
 #pragma unroll
-                for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+                for (int b = 0; b < 8; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
         };
         // end of tile x (the it-th of this CTA): planned flips (test harness), then the
         // accumulators go to TMEM buffer it & 1 and the epilogue is signalled
@@ -421,14 +583,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 const long long gtm = tm + g.off_i / BM, gtn = tn + g.off_j / BN;
                 if (gtm < g.plan_ntm && gtn < g.plan_ntn) {
                     const long long tix = gtn * g.plan_ntm + gtm;
-                    const int lo = g.plan_ptr[tix], hi = g.plan_ptr[tix + 1];
+                    const int lo = ld_ro(g.plan_ptr + tix), hi = ld_ro(g.plan_ptr + tix + 1);
                     for (int f = lo; f < hi; f++) {
-                        const long long li = g.plan_i[f] - g.off_i - tm * BM, lj = g.plan_j[f] - g.off_j - tn * BN;
-                        const int bit = g.plan_bit[f];
+                        const long long li = ld_ro(g.plan_i + f) - g.off_i - tm * BM;
+                        const long long lj = ld_ro(g.plan_j + f) - g.off_j - tn * BN;
+                        const int bit = ld_ro(g.plan_bit + f);
 #pragma unroll
-                        for (int a = 0; a < 8; a++)
+                        for (int a = 0; a < 4; a++)
 #pragma unroll
-                            for (int b = 0; b < 4; b++)
+                            for (int b = 0; b < 8; b++)
 #pragma unroll
                                 for (int e = 0; e < 2; e++)
                                     if (row_of(a) == li && col_of(b, e) == lj) acc[a][b][e] = flip_bit(acc[a][b][e], bit);
@@ -436,14 +599,30 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 }
             }
             const int buf = it & 1;
+            WS_T(te0);
             if (it >= 2) mbar_wait(&acc_empty[buf], (unsigned)(((it >> 1) - 1) & 1));
+            if (warp == 0 && lane == 0) WS_ADD(WP_MMA_WAIT_EMPTYACC, te0);
+            WS_T(ts0);
             tc_fence_after();
-            const unsigned tb = tbase + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)(buf * 256 + (warp >> 2) * 128);
+            const unsigned tb = tbase + ((unsigned)(32 * wm) << 16) + (unsigned)(buf * 256 + wn * 128);
 #pragma unroll
-            for (int a = 0; a < 8; a++) tmem_st8d(tb + 16 * a, &acc[a][0][0]);
+            for (int p = 0; p < 2; p++) {
+                // repetitions r = 2 b + e: 0..7 (b < 4) and 8..15 (b >= 4)
+                double lo0[8], hi0[8], lo1[8], hi1[8];
+#pragma unroll
+                for (int r = 0; r < 8; r++) {
+                    lo0[r] = acc[2 * p][r >> 1][r & 1];
+                    hi0[r] = acc[2 * p + 1][r >> 1][r & 1];
+                    lo1[r] = acc[2 * p][4 + (r >> 1)][r & 1];
+                    hi1[r] = acc[2 * p + 1][4 + (r >> 1)][r & 1];
+                }
+                tmem_st_pair8(tb + ((unsigned)(16 * p) << 16), lo0, hi0);
+                tmem_st_pair8(tb + ((unsigned)(16 * p) << 16) + 64, lo1, hi1);
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_full[buf]);
+            if (warp == 0 && lane == 0) WS_ADD(WP_MMA_TMEMST, ts0);
         };
         if (ktiles == 0) {  // alpha == 0 or K == 0: zero accumulators, epilogue only
             int it = 0;
@@ -455,6 +634,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             // The ring of operand stages runs across tile boundaries: slot st of round `phase`
             // holds the next k-tile.  The loop is unrolled over the slots so every fragment
             // address is one of the 8 FragAddr offsets plus an immediate (as in gemm_kernel).
+            WS_T(tm0);
             long long x = blockIdx.x;
             int it = 0, kt = 0;
             unsigned phase = 0;
@@ -464,19 +644,21 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
 #pragma unroll
                 for (int st = 0; st < WS_STAGES; st++) {
                     if (!done) {
+                        WS_T(tf0);
                         mbar_wait(&full_bar[st], phase);
+                        if (warp == 0 && lane == 0) WS_ADD(WP_MMA_WAIT_FULL, tf0);
                         const double *a_s = smem + st * WS_STAGE_EL, *b_s = a_s + TILE_EL;
 #pragma unroll
                         for (int kk = 0; kk < BK / 4; kk++) {
-                            double af[8], bf[4];
+                            double af[4], bf[8];
 #pragma unroll
-                            for (int f = 0; f < 8; f++) af[f] = a_s[fA(f, kk)];
+                            for (int f = 0; f < 4; f++) af[f] = a_s[fA(f, kk)];
 #pragma unroll
-                            for (int f = 0; f < 4; f++) bf[f] = b_s[fB(f, kk)];
+                            for (int f = 0; f < 8; f++) bf[f] = b_s[fB(f, kk)];
 #pragma unroll
-                            for (int a = 0; a < 8; a++)
+                            for (int a = 0; a < 4; a++)
 #pragma unroll
-                                for (int b = 0; b < 4; b++) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+                                for (int b = 0; b < 8; b++) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
                         }
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&empty_bar[st]);
@@ -492,6 +674,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 }
                 phase ^= 1u;
             }
+            if (warp == 0 && lane == 0) WS_ADD(WP_MMA_TOTAL, tm0);
         }
     }
     tc_fence_before();
@@ -499,6 +682,57 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     if (warp == 13) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase) : "memory");
+    }
+}
+
+// ------------------------------------------------------------------ deferred correction
+// After gemm_ws_kernel<FT>: every located candidate (i, j) is recomputed from its definition,
+// y = alpha sum_k op(A)(i,k) op(B)(k,j) + beta C0_ij (reading R6; one CTA per candidate, the K
+// range split over its 8 warps, fixed-order combination), and replaced iff it is the single
+// located error or differs from y beyond its rounding bound (reading R7); the report entry is
+// written for every replacement.  Runs on the GEMM's stream, so C is final when it starts.
+constexpr int CORR_THREADS = 256;
+template <bool KCA, bool KCB>
+__global__ void __launch_bounds__(CORR_THREADS) correct_kernel(const __grid_constant__ GemmArgs g) {
+    __shared__ double ps[CORR_THREADS / 32], psa[CORR_THREADS / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long n = min((long long)g.pend->count, g.pend_cap);
+    const double aa = fabs(g.alpha), ab = fabs(g.beta);
+    for (long long q = blockIdx.x; q < n; q += gridDim.x) {
+        const Pending pe = g.pend_entries[q];
+        double s = 0.0, sa = 0.0;
+        for (long long k = tid; k < g.K; k += CORR_THREADS) {
+            const double a = ld_ro(gaddr<KCA>(g.A, g.lda, pe.i, k));
+            const double b = ld_ro(gaddr<KCB>(g.B, g.ldb, pe.j, k));
+            s = fma(a, b, s);
+            sa = fma(fabs(a), fabs(b), sa);
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+            s += __shfl_xor_sync(0xffffffffu, s, off);
+            sa += __shfl_xor_sync(0xffffffffu, sa, off);
+        }
+        if (lane == 0) { ps[warp] = s; psa[warp] = sa; }
+        __syncthreads();
+        if (tid == 0) {
+            s = 0.0; sa = 0.0;
+            for (int w = 0; w < CORR_THREADS / 32; w++) { s += ps[w]; sa += psa[w]; }
+            const double y = g.beta == 0.0 ? g.alpha * s : fma(g.alpha, s, g.beta * pe.c0);
+            const double eb = 4.0 * U_ROUND * (double)(g.K + 3) * (aa * sa + ab * fabs(pe.c0));
+            if (pe.single || !(fabs(pe.cur - y) <= eb)) {
+                g.C[pe.i + pe.j * g.ldc] = y;  // correction (reading R6: the recomputed element)
+                const unsigned long long p = atomicAdd(&g.rep->count, 1ull);
+                if ((long long)p < g.rep_cap) {
+                    Correction cr;
+                    cr.tile_m = (pe.i + g.off_i) / BM; cr.tile_n = (pe.j + g.off_j) / BN;
+                    cr.i = pe.i + g.off_i; cr.j = pe.j + g.off_j;
+                    cr.residual = pe.residual;
+                    cr.kind = pe.single ? 1 : 2; cr.pad = 0;
+                    g.rep_entries[p] = cr;
+                }
+            }
+        }
+        __syncthreads();
     }
 }
 
