@@ -193,9 +193,7 @@ int sm_count() {
     return n;
 }
 
-// Persistent warp-specialized kernel (ftblas_ws.cuh): one CTA per SM over all tiles.  C0 and C
-// move through TMA (box 128 rows x 64 columns, no swizzle, zero fill) when C is 16-byte aligned
-// with an even ldc; otherwise vecC = 0 tells the kernel to use its copy fallback.
+// Persistent warp-specialized kernel (ftblas_ws.cuh): one CTA per SM over all tiles.
 cudaError_t launch_ws_any(const void *kern, GemmArgs g, const CUtensorMap &ma, const CUtensorMap &mb, long long tiles,
                           cudaStream_t s);
 
@@ -251,7 +249,9 @@ bool make_operand_map(CUtensorMap *m, const double *X, long long ld, long long M
     return r == CUDA_SUCCESS;
 }
 
-// Tensor map of C for the persistent kernel's epilogue: dims {M, N}, box {128, 64}, no swizzle.
+// Tensor map of C for the persistent kernel's epilogue: dims {M, N}, box {128, 32}, no swizzle,
+// zero fill; false (the kernel then copies with plain L2-only accesses) if C is not 16-byte
+// aligned or ldc is odd.
 bool make_c_map(CUtensorMap *m, const double *C, long long ldc, long long M, long long N) {
     std::memset(m, 0, sizeof(*m));
     EncodeTiledFn fn = encode_tiled();
@@ -259,7 +259,7 @@ bool make_c_map(CUtensorMap *m, const double *C, long long ldc, long long M, lon
     if (M >= (1ll << 31) || N >= (1ll << 31)) return false;
     const cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)N};
     const cuuint64_t strides[1] = {(cuuint64_t)ldc * 8};
-    const cuuint32_t box[2] = {128u, 64u};
+    const cuuint32_t box[2] = {128u, (cuuint32_t)WS_QCOLS};
     const cuuint32_t estr[2] = {1u, 1u};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(C), dims, strides, box, estr,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

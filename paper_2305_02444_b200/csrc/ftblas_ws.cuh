@@ -22,28 +22,41 @@
 // 32 (w % 4) + 16 p + [0, 16) and a row's 64 doubles of warp column w / 4 fill TMEM columns
 // buf * 256 + (w / 4) * 128 + [0, 128).  Epilogue warp ew (= its TMEM sub-partition) therefore
 // owns rows 32 ew .. +31, one row per thread, and reads its row 8 columns at a time.
-// C0 comes in and the verified tile goes out through a 64 KB shared buffer (half a tile) with
-// TMA (bulk tensor load / store), so the epilogue issues no L1-allocating global loads: with
-// ~200 KB of shared memory in use, L1-allocating loads running beside the DMMA mainloop
-// corrupted accumulators ("L1-allocating loads beside the DMMA stream").
+// With the lane = row layout a warp's C0 load / C store of one column covers 32 consecutive
+// rows (256 contiguous bytes), so the epilogue moves C with plain coalesced L2-only accesses
+// (ld/st.global.cg) and all shared memory goes to a 3-stage operand ring.  No L1-allocating
+// loads and no K-long recomputation run beside the DMMA mainloop (corrections are deferred to
+// correct_kernel): with ~200 KB of shared memory in use, long streams of L1-allocating loads
+// beside the mainloop corrupted accumulators.
 #pragma once
 #include "ftblas_kernels.cuh"
 
 namespace ftb {
 
 constexpr int WS_THREADS = 512;                 // 8 MMA + 4 epilogue + 4 producer-group warps
+// Warp roles: warps 12..15 producer group; the epilogue warpgroup first (warps 0..3) and the MMA
+// warps 4..11 by default (-DFTB_WS_EPI_LAST: MMA 0..7, epilogue 8..11).  A warp's TMEM
+// sub-partition is warp % 4 either way.
+#ifdef FTB_WS_EPI_LAST
+#define WS_IS_EPI(w) ((w) >= 8)
+#define WS_MMA_IDX(w) (w)
+#else
+#define WS_IS_EPI(w) ((w) < 4)
+#define WS_MMA_IDX(w) ((w) - 4)
+#endif
 #ifndef FTB_WS_STAGES
 #define FTB_WS_STAGES 2
 #endif
 constexpr int WS_STAGES = FTB_WS_STAGES;
 constexpr int WS_STAGE_EL = 2 * TILE_EL;        // A 128 x BK | B 128 x BK
-constexpr int WS_CBUF_EL = 64 * BM;             // C staging: 64 columns x 128 rows (half a tile)
-constexpr int WS_SMEM = (WS_STAGES * WS_STAGE_EL + WS_CBUF_EL) * 8 + 1024;
+constexpr int WS_QCOLS = 32;                     // C staging: quarter tiles of 32 columns x 128 rows,
+constexpr int WS_CBUF_EL = WS_QCOLS * BM;        // double-buffered (TMA load / store)
+constexpr int WS_SMEM = (WS_STAGES * WS_STAGE_EL + 2 * WS_CBUF_EL) * 8 + 1024;
 
 // setmaxnreg split of the 64 K registers (one CTA per SM)
 template <bool FT>
 struct WsRegs {
-    static constexpr int MMA = FT ? 184 : 200, EPI = FT ? 104 : 72, PROD = FT ? 40 : 32;
+    static constexpr int MMA = FT ? 192 : 200, EPI = FT ? 96 : 72, PROD = 32;
     static_assert(256 * MMA + 128 * EPI + 128 * PROD <= 65536,
                   "setmaxnreg budget exceeds the register file of one CTA per SM");
 };
@@ -131,7 +144,17 @@ __device__ __forceinline__ void tmem_ld8d(unsigned taddr, double *v) {
     for (int q = 0; q < 8; q++) v[q] = __hiloint2double(w[2 * q + 1], w[2 * q]);
 }
 
-// TMA of the C staging buffer: box {128 rows, 64 columns} of C (column-major, dense in smem)
+// C0 / C of the epilogue: TMA of quarter tiles (box {128 rows, 32 columns}, dense
+// [column][row] in shared memory); fallback (C not 16-byte aligned or odd ldc): L2-only loads
+// and stores (no L1 allocation, see the file comment).
+__device__ __forceinline__ double ld_c(const double *p) {
+    double v;
+    asm volatile("ld.global.cg.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_c(double *p, double v) {
+    asm volatile("st.global.cg.f64 [%0], %1;\n" ::"l"(p), "d"(v) : "memory");
+}
 __device__ __forceinline__ void tma_load_c(double *dst, const CUtensorMap *map, unsigned long long *bar, int row0,
                                            int col0) {
     asm volatile(
@@ -174,15 +197,13 @@ struct WsSide {
     double nrm_row[BM], nrm_col[BN], pre_r[BM], pre_s[BN], nrm_max[2];
 };
 
-// GemmArgs.vecC != 0 and a tensor map for C (tmC) <=> C0 / C move by TMA; else the epilogue
-// copies the staging buffer with L2-only loads and plain stores.
 template <bool KCA, bool KCB, bool TMA, bool FT>
 __global__ void __launch_bounds__(WS_THREADS, 1)
     gemm_ws_kernel(const __grid_constant__ GemmArgs g, const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmC) {
     extern __shared__ __align__(1024) double smem_raw[];
     __shared__ __align__(8) unsigned long long full_bar[WS_STAGES], empty_bar[WS_STAGES], acc_full[2], acc_empty[2],
-        c0_bar;
+        c0_full[2];
     __shared__ unsigned tmem_base_sh;
     __shared__ WsSide side;
     __shared__ double red_c[4][BN], dres[BM];  // column partials per epilogue warp (32 rows each)
@@ -190,7 +211,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     __shared__ int flags[2 + BM + BN];
     __shared__ int rflag[BM], cflag[BN];
     double *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) / 8u;
-    double *cbuf = smem + WS_STAGES * WS_STAGE_EL;  // [64 columns][128 rows]
+    double *cbuf = smem + WS_STAGES * WS_STAGE_EL;  // 2 x [32 columns][128 rows]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long ntm = (g.M + BM - 1) / BM, ntn = (g.N + BN - 1) / BN, ntiles = ntm * ntn;
     const int ktiles = (g.alpha == 0.0) ? 0 : (int)((g.K + BK - 1) / BK);
@@ -204,8 +225,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         for (int b = 0; b < 2; b++) {
             mbar_init(&acc_full[b], 8);      // MMA warps: accumulators in TMEM
             mbar_init(&acc_empty[b], 4);     // epilogue warps: buffer read
+            mbar_init(&c0_full[b], 1);       // C0 quarter tile in cbuf[b] (TMA, expect_tx)
         }
-        mbar_init(&c0_bar, 1);               // C0 half-tile TMA (expect_tx by the issuing thread)
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == 13) {  // TMEM: all 512 columns (two accumulator buffers); one CTA per SM
@@ -258,10 +279,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 }
             }
         }
-    } else if (warp >= 8) {
+    } else if (WS_IS_EPI(warp)) {
         // ------------------------------------------------------------------ epilogue
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(WsRegs<FT>::EPI));
-        const int ew = warp - 8, et = tid - 256;  // epilogue warp (= TMEM sub-partition), thread
+        const int ew = warp & 3, et = 32 * ew + lane;  // epilogue warp (= TMEM sub-partition), thread
         auto epi_bar = [&]() { asm volatile("bar.sync 2, 128;\n" ::: "memory"); };
         // beta classes decided once on the integer pipe (FP64 instructions beside the DMMA stream
         // wait for the tensor pipe: every one in the per-element code costs)
@@ -273,55 +294,60 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         // doubles of TMEM chunk j of warp column wn (q = 4 e + t)
         const int row = frag_mn<KCA>(32 * ew, lane >> 3, lane & 7);
         auto col_of = [&](int wn, int j, int q) { return frag_mn<KCB>(64 * wn, j, 2 * (q & 3) + (q >> 2)); };
+        // C staging: quarter q of a tile = columns 32 q .. +31 = TMEM chunks (h = q / 2, j = 4 (q % 2)
+        // .. +3) of every row (both column layouts), in cbuf[slot] ([32 columns][128 rows]).  The
+        // loads / stores are TMA (thread 0) when C has a tensor map, else L2-only copies.
         const bool tma_c = g.vecC != 0;
         const bool need_c0 = !beta0;
-        unsigned c0_phase = 0;
-        // C0 half h of the tile at (m0, n0) -> cbuf: TMA by thread 0, or L2-only loads by all
-        auto load_c0 = [&](long long m0, long long n0, int h) {
+        unsigned c0_phase[2] = {0u, 0u};
+        auto qbuf = [&](int slot) { return cbuf + slot * WS_CBUF_EL; };
+        auto load_c0 = [&](long long m0, long long n0, int q, int slot) {  // issue (TMA) / copy
             if (tma_c) {
                 if (et == 0) {
-                    mbar_arrive_expect_tx(&c0_bar, (unsigned)(WS_CBUF_EL * 8));
-                    tma_load_c(cbuf, &tmC, &c0_bar, (int)m0, (int)(n0 + 64 * h));
+                    mbar_arrive_expect_tx(&c0_full[slot], (unsigned)(WS_CBUF_EL * 8));
+                    tma_load_c(qbuf(slot), &tmC, &c0_full[slot], (int)m0, (int)(n0 + WS_QCOLS * q));
                 }
             } else {
                 const long long gi = m0 + et;
-                for (int c = 0; c < 64; c++) {
-                    const long long gj = n0 + 64 * h + c;
-                    cbuf[c * BM + et] = (gi < g.M && gj < g.N) ? __ldcg(g.C + gi + gj * g.ldc) : 0.0;
+                for (int c = 0; c < WS_QCOLS; c++) {
+                    const long long gj = n0 + WS_QCOLS * q + c;
+                    qbuf(slot)[c * BM + et] = (gi < g.M && gj < g.N) ? ld_c(g.C + gi + gj * g.ldc) : 0.0;
                 }
             }
         };
-        auto wait_c0 = [&]() {
+        auto wait_c0 = [&](int slot) {
             if (tma_c) {
-                mbar_wait(&c0_bar, c0_phase);
-                c0_phase ^= 1u;
+                mbar_wait(&c0_full[slot], c0_phase[slot]);
+                c0_phase[slot] ^= 1u;
             } else {
                 epi_bar();
             }
         };
-        // cbuf (half h) -> C of the tile at (m0, n0); the buffer is reusable when this returns
-        auto store_c = [&](long long m0, long long n0, int h, long long mvalid, long long nvalid) {
+        // cbuf[slot] -> quarter q of C; the slot can be refilled once this returns (thread 0 waits
+        // for the TMA to have read it; the barrier publishes that to the other threads)
+        auto store_q = [&](long long m0, long long n0, int q, int slot, long long mvalid, long long nvalid) {
             if (tma_c) {
                 fence_proxy_async_smem();  // generic-proxy writes of cbuf -> visible to the TMA
                 epi_bar();
                 if (et == 0) {
-                    tma_store_c(&tmC, cbuf, (int)m0, (int)(n0 + 64 * h));
+                    tma_store_c(&tmC, qbuf(slot), (int)m0, (int)(n0 + WS_QCOLS * q));
                     tma_store_wait_read();
                 }
                 epi_bar();
             } else {
                 epi_bar();
                 if (et < mvalid)
-                    for (int c = 0; c < 64 && 64 * h + c < nvalid; c++)
-                        g.C[(m0 + et) + (n0 + 64 * h + c) * g.ldc] = cbuf[c * BM + et];
+                    for (int c = 0; c < WS_QCOLS && WS_QCOLS * q + c < nvalid; c++)
+                        st_c(g.C + (m0 + et) + (n0 + WS_QCOLS * q + c) * g.ldc, qbuf(slot)[c * BM + et]);
                 epi_bar();
             }
         };
         int it = 0;
-        if (blockIdx.x < ntiles && need_c0) {
+        if (blockIdx.x < ntiles && need_c0) {  // C0 quarters 0, 1 of the first tile
             long long tm, tn;
             tile_coords(blockIdx.x, ntm, ntn, tm, tn);
-            load_c0(tm * BM, tn * BN, 0);
+            load_c0(tm * BM, tn * BN, 0, 0);
+            load_c0(tm * BM, tn * BN, 1, 1);
         }
         for (long long x = blockIdx.x; x < ntiles; x += gridDim.x, it++) {
             long long tm, tn;
@@ -329,6 +355,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             const long long m0 = tm * BM, n0 = tn * BN;
             const long long mvalid = min((long long)BM, g.M - m0), nvalid = min((long long)BN, g.N - n0);
             const bool rowok = row < mvalid;
+            const bool has_next = x + gridDim.x < ntiles;
+            long long m0n = 0, n0n = 0;
+            if (has_next) {
+                long long tm2, tn2;
+                tile_coords(x + gridDim.x, ntm, ntn, tm2, tn2);
+                m0n = tm2 * BM; n0n = tn2 * BN;
+            }
             if (FT) {  // side data of this tile (loads overlap the wait for the accumulators)
                 const long long gi = m0 + et, gj = n0 + et;
                 side.nrm_row[et] = et < mvalid ? ld_ro(g.fin_nrmA + gi) : 0.0;
@@ -349,111 +382,121 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             WS_T(tp1);
             tc_fence_after();
             const unsigned tb = tbase + ((unsigned)(32 * ew) << 16) + (unsigned)(buf * 256);
-            // ---- pass 1, half h = warp column wn: out, the row sum, column partials.  One chunk =
-            // 8 doubles of this thread's row; the row sum keeps 8 independent partials (one per
-            // chunk position q, combined in fixed order after the tile) so the FP64 adds do not
-            // form one 128-long dependency chain.
+            // ---- pass 1, quarter by quarter, chunk = 8 doubles of this thread's row: out, the row
+            // sum (8 independent partials, one per chunk position q, combined in fixed order after
+            // the tile, so the FP64 adds do not form one 128-long dependency chain) and the column
+            // partials.  FT: out goes back into TMEM; non-FT: into cbuf, stored per quarter.
             double rsq[8];
 #pragma unroll
             for (int q = 0; q < 8; q++) rsq[q] = 0.0;
             unsigned rm = 0u;
-            auto chunk = [&](auto mode_c, int h, int j) {
+            auto pass1 = [&](auto mode_c) {
                 constexpr int MODE = decltype(mode_c)::value;  // 0: beta = 0, 1: beta = 1, 2: other
-                double v[8], cs[8];
-                unsigned cm[8];
-                tmem_ld8d(tb + h * 128 + 16 * j, v);
-#pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    const int col = col_of(h, j, q);          // column in the tile
-                    const int cl = col - 64 * h;               // column in the half
-                    double o, d;
-                    cm[q] = 0u;
-                    if (MODE == 0) {
-                        o = g.alpha * v[q];
-                        d = o;
-                    } else {
-                        const double c0 = cbuf[cl * BM + row];  // 0 outside M x N (TMA zero fill)
-                        const double tt = MODE == 1 ? c0 : g.beta * c0;
-                        o = fma(g.alpha, v[q], tt);
-                        d = o - tt;
-                        if (FT) {
-                            const unsigned hw = (unsigned)__double2hiint(c0) & 0x7fffffffu;
-                            rm = max(rm, hw);
-                            cm[q] = hw;
-                        }
+#pragma unroll 1
+                for (int qq = 0; qq < 4; qq++) {
+                    const int slot = qq & 1;
+                    double *cb = qbuf(slot);
+                    if (MODE != 0) {
+                        WS_T(tc0);
+                        wait_c0(slot);
+                        if (et == 0) WS_ADD(WP_EPI_WAIT_C0, tc0);
                     }
-                    if (FT) {
-                        d = (rowok && col < nvalid) ? d : 0.0;
-                        rsq[q] += d;
-                        cs[q] = d;
-                        v[q] = o;
-                    } else {
-                        cbuf[cl * BM + row] = o;
-                    }
-                }
-                if (FT) {
-                    tmem_st8d(tb + h * 128 + 16 * j, v);
-                    // column sums over this warp's 32 rows: transposing butterfly over lane bits
-                    // 4, 3, 2 (8 -> 1 value per lane), then plain over bits 1, 0
+#pragma unroll 1
+                    for (int jj = 0; jj < 4; jj++) {
+                        const int h = qq >> 1, j = 4 * (qq & 1) + jj;
+                        double v[8], cs[8];
+                        unsigned cm[8];
+#ifdef FTB_DBG_NOLDTM
 #pragma unroll
-                    for (int off = 16; off >= 4; off >>= 1) {
-                        const bool up = (lane & off) != 0;
-                        const int hh = off / 4;  // 4, 2, 1 values kept
+                        for (int q = 0; q < 8; q++) v[q] = (double)(q + j);
+#else
+                        tmem_ld8d(tb + h * 128 + 16 * j, v);
+#endif
 #pragma unroll
-                        for (int i2 = 0; i2 < 4; i2++) {
-                            if (i2 < hh) {
-                                const double send = up ? cs[i2] : cs[i2 + hh];
-                                const double keep = up ? cs[i2 + hh] : cs[i2];
-                                cs[i2] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-                                if (MODE != 0) {
-                                    const unsigned ms = up ? cm[i2] : cm[i2 + hh];
-                                    const unsigned mk = up ? cm[i2 + hh] : cm[i2];
-                                    cm[i2] = max(mk, __shfl_xor_sync(0xffffffffu, ms, off));
+                        for (int q = 0; q < 8; q++) {
+                            const int col = col_of(h, j, q);
+                            const int cl = col - WS_QCOLS * qq;  // column in the quarter
+                            double o, d;
+                            cm[q] = 0u;
+                            if (MODE == 0) {
+                                o = g.alpha * v[q];
+                                d = o;
+                            } else {
+                                const double c0 = cb[cl * BM + row];  // 0 outside M x N (zero fill)
+                                const double tt = MODE == 1 ? c0 : g.beta * c0;
+#ifdef FTB_DBG_NOFMA
+                                o = __longlong_as_double(__double_as_longlong(v[q]) ^ __double_as_longlong(tt));
+#else
+                                o = fma(g.alpha, v[q], tt);
+#endif
+                                d = o - tt;
+                                if (FT) {
+                                    const unsigned hw = (unsigned)__double2hiint(c0) & 0x7fffffffu;
+                                    rm = max(rm, hw);
+                                    cm[q] = hw;
                                 }
+                            }
+                            if (FT) {
+                                d = (rowok && col < nvalid) ? d : 0.0;
+                                rsq[q] += d;
+                                cs[q] = d;
+                                v[q] = o;
+                            } else {
+                                cb[cl * BM + row] = o;
+                            }
+                        }
+                        if (FT) {
+                            tmem_st8d(tb + h * 128 + 16 * j, v);
+                            // column sums over this warp's 32 rows: transposing butterfly over lane
+                            // bits 4, 3, 2 (8 -> 1 value per lane), then plain over bits 1, 0
+#pragma unroll
+                            for (int off = 16; off >= 4; off >>= 1) {
+                                const bool up = (lane & off) != 0;
+                                const int hh = off / 4;  // 4, 2, 1 values kept
+#pragma unroll
+                                for (int i2 = 0; i2 < 4; i2++) {
+                                    if (i2 < hh) {
+                                        const double send = up ? cs[i2] : cs[i2 + hh];
+                                        const double keep = up ? cs[i2 + hh] : cs[i2];
+                                        cs[i2] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                                        if (MODE != 0) {
+                                            const unsigned ms = up ? cm[i2] : cm[i2 + hh];
+                                            const unsigned mk = up ? cm[i2 + hh] : cm[i2];
+                                            cm[i2] = max(mk, __shfl_xor_sync(0xffffffffu, ms, off));
+                                        }
+                                    }
+                                }
+                            }
+                            cs[0] += __shfl_xor_sync(0xffffffffu, cs[0], 2);
+                            cs[0] += __shfl_xor_sync(0xffffffffu, cs[0], 1);
+                            if (MODE != 0) {
+                                cm[0] = max(cm[0], __shfl_xor_sync(0xffffffffu, cm[0], 2));
+                                cm[0] = max(cm[0], __shfl_xor_sync(0xffffffffu, cm[0], 1));
+                            }
+                            if ((lane & 3) == 0) {
+                                const int q = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+                                const int col = col_of(h, j, q);
+                                red_c[ew][col] = cs[0];
+                                redm_c[ew][col] = cm[0];
                             }
                         }
                     }
-                    cs[0] += __shfl_xor_sync(0xffffffffu, cs[0], 2);
-                    cs[0] += __shfl_xor_sync(0xffffffffu, cs[0], 1);
-                    if (MODE != 0) {
-                        cm[0] = max(cm[0], __shfl_xor_sync(0xffffffffu, cm[0], 2));
-                        cm[0] = max(cm[0], __shfl_xor_sync(0xffffffffu, cm[0], 1));
+                    if (!FT) {
+                        store_q(m0, n0, qq, slot, mvalid, nvalid);  // the slot is free afterwards
+                    } else if (MODE != 0) {
+                        epi_bar();  // every thread done reading this C0 quarter
                     }
-                    if ((lane & 3) == 0) {
-                        const int q = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-                        const int col = col_of(h, j, q);
-                        red_c[ew][col] = cs[0];
-                        redm_c[ew][col] = cm[0];
+                    // refill the slot: quarter qq + 2 of this tile, or (non-FT) quarter qq - 2 of the
+                    // next one (FT: the next tile's C0 waits until pass 2 has used the slots)
+                    if (MODE != 0) {
+                        if (qq < 2) load_c0(m0, n0, qq + 2, slot);
+                        else if (!FT && has_next) load_c0(m0n, n0n, qq - 2, slot);
                     }
                 }
             };
-#pragma unroll 1
-            for (int h = 0; h < 2; h++) {
-                if (need_c0) {
-                    WS_T(tc0);
-                    wait_c0();
-                    if (et == 0) WS_ADD(WP_EPI_WAIT_C0, tc0);
-                }
-                if (bmode == 0) {
-#pragma unroll 1
-                    for (int j = 0; j < 8; j++) chunk(IntC<0>{}, h, j);
-                } else if (bmode == 1) {
-#pragma unroll 1
-                    for (int j = 0; j < 8; j++) chunk(IntC<1>{}, h, j);
-                } else {
-#pragma unroll 1
-                    for (int j = 0; j < 8; j++) chunk(IntC<2>{}, h, j);
-                }
-                if (!FT) {
-                    WS_T(ts0);
-                    store_c(m0, n0, h, mvalid, nvalid);
-                    if (et == 0) WS_ADD(WP_EPI_STORE, ts0);
-                    if (h == 0 && need_c0) load_c0(m0, n0, 1);
-                } else if (h == 0 && need_c0) {
-                    epi_bar();  // every thread done reading C0 half 0
-                    load_c0(m0, n0, 1);
-                }
-            }
+            if (bmode == 0) pass1(IntC<0>{});
+            else if (bmode == 1) pass1(IntC<1>{});
+            else pass1(IntC<2>{});
             if (et == 0) WS_ADD(WP_EPI_PASS1, tp1);
             WS_T(tv0);
             if (FT) {
@@ -519,7 +562,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                                         Pending pe;
                                         pe.i = m0 + row; pe.j = n0 + col;
                                         pe.cur = v[q];
-                                        pe.c0 = beta0 ? 0.0 : __ldcg(g.C + (m0 + row) + (n0 + col) * g.ldc);
+                                        pe.c0 = beta0 ? 0.0 : ld_c(g.C + (m0 + row) + (n0 + col) * g.ldc);
                                         pe.residual = dres[row];
                                         pe.single = single ? 1 : 0; pe.pad = 0;
                                         g.pend_entries[p] = pe;
@@ -530,31 +573,34 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 }
                 if (et == 0) WS_ADD(WP_EPI_VERIFY, tv0);
                 WS_T(tq0);
-                // ---- pass 2: the verified tile -> cbuf -> C, half by half
+                // ---- pass 2: the verified tile -> cbuf -> C, quarter by quarter (double-buffered);
+                // then C0 quarters 0, 1 of the next tile
 #pragma unroll 1
-                for (int h = 0; h < 2; h++) {
+                for (int qq = 0; qq < 4; qq++) {
+                    const int slot = qq & 1;
+                    double *cb = qbuf(slot);
 #pragma unroll 1
-                    for (int j = 0; j < 8; j++) {
+                    for (int jj = 0; jj < 4; jj++) {
+                        const int h = qq >> 1, j = 4 * (qq & 1) + jj;
                         double v[8];
                         tmem_ld8d(tb + h * 128 + 16 * j, v);
 #pragma unroll
-                        for (int q = 0; q < 8; q++) cbuf[(col_of(h, j, q) - 64 * h) * BM + row] = v[q];
+                        for (int q = 0; q < 8; q++) cb[(col_of(h, j, q) - WS_QCOLS * qq) * BM + row] = v[q];
                     }
                     WS_T(ts1);
-                    store_c(m0, n0, h, mvalid, nvalid);
+                    store_q(m0, n0, qq, slot, mvalid, nvalid);
                     if (et == 0) WS_ADD(WP_EPI_STORE, ts1);
+                }
+                if (need_c0 && has_next) {
+                    load_c0(m0n, n0n, 0, 0);
+                    load_c0(m0n, n0n, 1, 1);
                 }
                 if (et == 0) WS_ADD(WP_EPI_PASS2, tq0);
             }
-            // accumulator buffer read: hand it back to the MMA warps; C0 of the next tile
+            // accumulator buffer read: hand it back to the MMA warps
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[buf]);
-            if (need_c0 && x + gridDim.x < ntiles) {
-                long long tm2, tn2;
-                tile_coords(x + gridDim.x, ntm, ntn, tm2, tn2);
-                load_c0(tm2 * BM, tn2 * BN, 0);
-            }
             epi_bar();  // side data / flags / reductions of this tile consumed by every thread
             if (et == 0) WS_ADD(WP_EPI_TOTAL, tw0);
         }
@@ -562,7 +608,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     } else {
         // ------------------------------------------------------------------ MMA warps
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(WsRegs<FT>::MMA));
-        const int wm = warp & 3, wn = warp >> 2;  // rows 32 wm, columns 64 wn of the tile
+        const int mw = WS_MMA_IDX(warp);           // MMA warp index 0..7
+        const int wm = mw & 3, wn = mw >> 2;       // rows 32 wm, columns 64 wn of the tile
         const FragAddr<KCA> fA(wm * 32, lane);
         const FragAddr<KCB> fB(wn * 64, lane);
         auto row_of = [&](int a) { return frag_mn<KCA>(wm * 32, a, lane >> 2); };
@@ -601,7 +648,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             const int buf = it & 1;
             WS_T(te0);
             if (it >= 2) mbar_wait(&acc_empty[buf], (unsigned)(((it >> 1) - 1) & 1));
-            if (warp == 0 && lane == 0) WS_ADD(WP_MMA_WAIT_EMPTYACC, te0);
+            if (mw == 0 && lane == 0) WS_ADD(WP_MMA_WAIT_EMPTYACC, te0);
             WS_T(ts0);
             tc_fence_after();
             const unsigned tb = tbase + ((unsigned)(32 * wm) << 16) + (unsigned)(buf * 256 + wn * 128);
@@ -622,7 +669,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_full[buf]);
-            if (warp == 0 && lane == 0) WS_ADD(WP_MMA_TMEMST, ts0);
+            if (mw == 0 && lane == 0) WS_ADD(WP_MMA_TMEMST, ts0);
         };
         if (ktiles == 0) {  // alpha == 0 or K == 0: zero accumulators, epilogue only
             int it = 0;
@@ -646,7 +693,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                     if (!done) {
                         WS_T(tf0);
                         mbar_wait(&full_bar[st], phase);
-                        if (warp == 0 && lane == 0) WS_ADD(WP_MMA_WAIT_FULL, tf0);
+                        if (mw == 0 && lane == 0) WS_ADD(WP_MMA_WAIT_FULL, tf0);
                         const double *a_s = smem + st * WS_STAGE_EL, *b_s = a_s + TILE_EL;
 #pragma unroll
                         for (int kk = 0; kk < BK / 4; kk++) {
@@ -674,7 +721,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 }
                 phase ^= 1u;
             }
-            if (warp == 0 && lane == 0) WS_ADD(WP_MMA_TOTAL, tm0);
+            if (mw == 0 && lane == 0) WS_ADD(WP_MMA_TOTAL, tm0);
         }
     }
     tc_fence_before();

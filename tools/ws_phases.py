@@ -2,7 +2,7 @@
 (tools/dbg/ws_prof.so copied over the library).  Usage: python tools/ws_phases.py <workload> [ft|noft]"""
 import ctypes as ct, os, shutil, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-shutil.copy(os.path.join(ROOT, "tools", "dbg", "ws_prof.so"), os.path.join(ROOT, "paper_2305_02444_b200", "lib", "libftblas.so"))
+shutil.copy(os.path.join(ROOT, "tools", "dbg", os.environ.get("WS_PROF_SO", "ws_prof.so")), os.path.join(ROOT, "paper_2305_02444_b200", "lib", "libftblas.so"))
 sys.path.insert(0, ROOT)
 import numpy as np, torch
 import synthetic as syn
