@@ -10,7 +10,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "lib", "libftblas.so")
 SOURCES = [os.path.join(CSRC, "ftblas.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "ftblas_kernels.cuh"), os.path.join(ROOT, "include", "ftblas.h")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith(".cuh")] + \
+    [os.path.join(ROOT, "include", "ftblas.h"), os.path.abspath(__file__)]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

@@ -249,31 +249,12 @@ bool make_operand_map(CUtensorMap *m, const double *X, long long ld, long long M
     return r == CUDA_SUCCESS;
 }
 
-// Tensor map of C for the persistent kernel's epilogue: dims {M, N}, box {128, 32}, no swizzle,
-// zero fill; false (the kernel then copies with plain L2-only accesses) if C is not 16-byte
-// aligned or ldc is odd.
-bool make_c_map(CUtensorMap *m, const double *C, long long ldc, long long M, long long N) {
-    std::memset(m, 0, sizeof(*m));
-    EncodeTiledFn fn = encode_tiled();
-    if (!fn || !C || M <= 0 || N <= 0 || (reinterpret_cast<uintptr_t>(C) & 15) || (ldc & 1)) return false;
-    if (M >= (1ll << 31) || N >= (1ll << 31)) return false;
-    const cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)N};
-    const cuuint64_t strides[1] = {(cuuint64_t)ldc * 8};
-    const cuuint32_t box[2] = {128u, (cuuint32_t)WS_QCOLS};
-    const cuuint32_t estr[2] = {1u, 1u};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(C), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 cudaError_t launch_ws_any(const void *kern, GemmArgs g, const CUtensorMap &ma, const CUtensorMap &mb, long long tiles,
                           cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_SMEM);
     if (e != cudaSuccess) return e;
-    CUtensorMap mc;
-    if (!make_c_map(&mc, g.C, g.ldc, g.M, g.N)) g.vecC = 0;
     const unsigned grid = (unsigned)std::min<long long>(tiles, sm_count());
-    void *args[] = {&g, const_cast<CUtensorMap *>(&ma), const_cast<CUtensorMap *>(&mb), &mc};
+    void *args[] = {&g, const_cast<CUtensorMap *>(&ma), const_cast<CUtensorMap *>(&mb)};
     e = cudaLaunchKernel(kern, dim3(grid), dim3(WS_THREADS), args, WS_SMEM, s);
     ctx().launches++;
     return e;
