@@ -592,33 +592,6 @@ __device__ __forceinline__ void tile_coords(long long x, long long ntm, long lon
     tn = r / gm;
 }
 
-// One warp recomputes element (i,j) of op(A) op(B) from its definition:
-// s = sum_k op(A)(i,k) op(B)(k,j), sa = sum_k |op(A)(i,k)| |op(B)(k,j)|.
-template <bool KCA, bool KCB>
-__device__ void warp_recompute(const GemmArgs &g, long long i, long long j, double &s, double &sa) {
-    const int lane = threadIdx.x & 31;
-    s = 0.0; sa = 0.0;
-    for (long long k = lane; k < g.K; k += 32) {
-#if defined(FTB_DBG_NC)
-        const double a = __ldg(gaddr<KCA>(g.A, g.lda, i, k));
-        const double b = __ldg(gaddr<KCB>(g.B, g.ldb, j, k));
-#elif defined(FTB_DBG_CG)
-        const double a = __ldcg(gaddr<KCA>(g.A, g.lda, i, k));
-        const double b = __ldcg(gaddr<KCB>(g.B, g.ldb, j, k));
-#else
-        const double a = *gaddr<KCA>(g.A, g.lda, i, k);
-        const double b = *gaddr<KCB>(g.B, g.ldb, j, k);
-#endif
-        s = fma(a, b, s);
-        sa = fma(fabs(a), fabs(b), sa);
-    }
-#pragma unroll
-    for (int off = 16; off; off >>= 1) {
-        s += __shfl_xor_sync(0xffffffffu, s, off);
-        sa += __shfl_xor_sync(0xffffffffu, sa, off);
-    }
-}
-
 // Block = NTHREADS MMA threads (8 warps) + producer threads (Warps<NWN>::PT).  Thread 0 of the producer
 // issues the TMA boxes of each stage (and the bulk copies of the checksum-vector slices) and
 // arms the stage's `full` mbarrier with the byte count; MMA warps release stages through
@@ -1178,51 +1151,37 @@ __global__ void __launch_bounds__(Warps<NWN>::NT + Warps<NWN>::PT, NWN == 2 ? 2 
     const int nr = flags[0], nc = flags[1];
     const int nct = PAIR ? nc + peer_nc : nc;
     if (nr != 0 || nct != 0) {
-        // ---------------------------------------------------------- locate + correct (rare)
+        // ---------------------------------------------------------- locate (rare)
+        // candidates: (flagged rows, or all rows) x (this CTA's flagged columns, or all its
+        // columns when no column of the tile is flagged); none when only the peer has flags
+        // (readings R5, R7).  Each is listed with its stored value and C0 (C is stored after
+        // this); the K-long recomputation and the correction (reading R6) run after the GEMM in
+        // correct_kernel (ftblas_ws.cuh): a long recomputation beside DMMA mainloops running on
+        // the same SM (the co-resident pair CTA) corrupted their accumulators (DESIGN.md
+        // section 2), and one warp on a K-long strided dot product stalled the tile.
         if (tid == 0) {
             if (half == 0) {  // once per verification tile
                 atomicAdd(&g.rep->tiles_flagged, 1ull);
                 atomicAdd(&g.rep->rows_flagged, (unsigned long long)nr);
             }
             atomicAdd(&g.rep->cols_flagged, (unsigned long long)nc);
-            for (int x = 1; x < nr; x++)
-                for (int y = x; y > 0 && flags[2 + y - 1] > flags[2 + y]; y--) {
-                    const int t = flags[2 + y]; flags[2 + y] = flags[2 + y - 1]; flags[2 + y - 1] = t;
-                }
-            for (int x = 1; x < nc; x++)
-                for (int y = x; y > 0 && flags[130 + y - 1] > flags[130 + y]; y--) {
-                    const int t = flags[130 + y]; flags[130 + y] = flags[130 + y - 1]; flags[130 + y - 1] = t;
-                }
         }
-        bar_mma();
         const bool single = (nr == 1 && nct == 1);  // Huang-Abraham location (line 540)
-        // candidates: (flagged rows, or all rows) x (this CTA's flagged columns, or all its
-        // columns when no column of the tile is flagged); none when only the peer has flags
         const long long ncr = nr ? nr : mvalid, ncc = nct ? nc : nvalid;
-        for (long long q = warp; q < ncr * ncc; q += NT / 32) {
+        for (long long q = tid; q < ncr * ncc; q += NT) {
             const int r = nr ? flags[2 + (int)(q % ncr)] : (int)(q % ncr);
             const int c = nc ? flags[130 + (int)(q / ncr)] : (int)(q / ncr);
-            const long long gi = m0 + r, gj = n0 + c;
-            double s, sa;
-            warp_recompute<KCA, KCB>(g, gi, gj, s, sa);
-            const double c0 = beta0 ? 0.0 : g.C[gi + gj * g.ldc];  // C is stored after this phase
-            const double y = beta0 ? g.alpha * s : fma(g.alpha, s, g.beta * c0);
-            const double eb = 4.0 * U_ROUND * (double)(g.K + 3) * (aa * sa + ab * fabs(c0));
-            const double cur = tileS[r + c * LDT];
-            if (lane == 0 && (single || !(fabs(cur - y) <= eb))) {
-                tileS[r + c * LDT] = y;  // correction (reading R6: recompute the located element)
-                const unsigned long long p = atomicAdd(&g.rep->count, 1ull);
-                if ((long long)p < g.rep_cap) {
-                    Correction cr;
-                    cr.tile_m = tm + g.off_i / BM; cr.tile_n = tn + g.off_j / BN;  // the 128 x 128 tile
-                    cr.i = gi + g.off_i; cr.j = gj + g.off_j;
-                    cr.residual = dres[r];
-                    cr.kind = single ? 1 : 2; cr.pad = 0;
-                    g.rep_entries[p] = cr;
-                }
+            const unsigned long long p = atomicAdd(&g.pend->count, 1ull);
+            if ((long long)p < g.pend_cap) {
+                Pending pe;
+                pe.i = m0 + r; pe.j = n0 + c;
+                pe.cur = tileS[r + c * LDT];
+                pe.c0 = beta0 ? 0.0 : __ldcg(g.C + (m0 + r) + (n0 + c) * g.ldc);
+                pe.residual = dres[r];
+                pe.single = single ? 1 : 0; pe.pad = 0;
+                g.pend_entries[p] = pe;
             }
         }
-        bar_mma();
     }
     // coalesced store of the verified tile
     store_tile();
