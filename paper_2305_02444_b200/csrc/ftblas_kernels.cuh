@@ -1182,6 +1182,7 @@ __global__ void __launch_bounds__(Warps<NWN>::NT + Warps<NWN>::PT, NWN == 2 ? 2 
                 g.pend_entries[p] = pe;
             }
         }
+        bar_mma();  // every candidate's C0 read before the tile overwrites C
     }
     // coalesced store of the verified tile
     store_tile();

@@ -30,6 +30,9 @@
 // beside the mainloop corrupted accumulators.
 #pragma once
 #include "ftblas_kernels.cuh"
+#ifdef FTB_DBG_CORR
+#include <cstdio>
+#endif
 
 namespace ftb {
 
@@ -778,6 +781,10 @@ __global__ void __launch_bounds__(CORR_THREADS) correct_kernel(const __grid_cons
             for (int w = 0; w < CORR_THREADS / 32; w++) { s += ps[w]; sa += psa[w]; }
             const double y = g.beta == 0.0 ? g.alpha * s : fma(g.alpha, s, g.beta * pe.c0);
             const double eb = 4.0 * U_ROUND * (double)(g.K + 3) * (aa * sa + ab * fabs(pe.c0));
+#ifdef FTB_DBG_CORR
+            printf("corr q %lld i %lld j %lld cur %g c0 %g y %g single %d ldc %lld C %p K %lld\n", q, pe.i, pe.j, pe.cur, pe.c0, y,
+                   pe.single, g.ldc, (void *)g.C, g.K);
+#endif
             if (pe.single || !(fabs(pe.cur - y) <= eb)) {
                 g.C[pe.i + pe.j * g.ldc] = y;  // correction (reading R6: the recomputed element)
                 const unsigned long long p = atomicAdd(&g.rep->count, 1ull);
