@@ -321,7 +321,7 @@ def main():
         fb.ftblas_profile(True)
         fb.ftblas_profile_read()
         n0 = fb.ftblas_launch_count()
-        ms_step = timed(lambda: step(gemm_ft, True), K)
+        ms_step = timed(lambda: step(gemm_ft, True), K, warm=0)  # warmed above; profiled: exactly K steps
         launches = fb.ftblas_launch_count() - n0
         fb.ftblas_profile(False)
         enc_ms, gemm_ms, n_g = fb.ftblas_profile_read()
@@ -440,9 +440,11 @@ def main():
             cflops = 2.0 * cw.M * cw.N * cw.K
             ctf = lambda ms: cflops / (ms * 1e-3) / 1e12  # noqa: E731
             fb.ftblas_set_fault_plan(*cplan)
+            for _ in range(W):
+                cft()
             fb.ftblas_profile(True)
             fb.ftblas_profile_read()
-            c_err = timed(cft, K, warm=W)
+            c_err = timed(cft, K, warm=0)
             fb.ftblas_profile(False)
             _, c_gemm_ms, c_n = fb.ftblas_profile_read()
             crep = fb.ftblas_report_fetch(fb.Report(max(16, 2 * cw.n_flips)))
