@@ -578,6 +578,68 @@ def test_many_faulted_tiles_leave_neighbours_clean(tB, tiles):
         ft.ftblas_set_tile_policy("auto")
 
 
+@pytest.mark.parametrize("tiles", ["ws", "pair", "full"])
+def test_deep_k_faulted_tiles_no_spurious_flags(tiles):
+    """The case that corrupted accumulators of concurrently running tiles when a K-long one-warp
+    recomputation ran beside DMMA mainloops (4096^3 NT, 100 flips: ~10 extra tiles and hundreds
+    of extra rows / columns flagged): with the recomputation deferred to
+    correct_kernel, exactly the 100 planned flips are flagged (one row, one column each) and
+    located, in each of 3 repetitions."""
+    import torch
+    ft = _lib("gemm", tiles)
+    try:
+        w = syn.Workload("t", 4096, 4096, 4096, "N", "T", 1.5, -0.5, "uniform", True, seed=5)
+        d = syn.make_inputs(w)
+        plan = syn.fault_plan(w.M, w.N, 100, 17)
+        A_t, pA = to_dev(d["A"]); B_t, pB = to_dev(d["B"])
+        want = sorted((int(i), int(j), 1) for i, j in zip(plan[0], plan[1]))
+        ft.ftblas_set_fault_plan(*plan)
+        for _ in range(3):
+            C_t, pC = to_dev(d["C"])
+            rep = ft.Report(4096)
+            ft.ftblas_dgemm(w.transA, w.transB, w.M, w.N, w.K, w.alpha, pA, d["lda"], pB, d["ldb"],
+                            w.beta, pC, d["ldc"], rep)
+            torch.cuda.synchronize()
+            assert (rep.count, rep.tiles_flagged, rep.rows_flagged, rep.cols_flagged) == (100, 100, 100, 100)
+            assert sorted((e["i"], e["j"], e["kind"]) for e in rep.entries()) == want
+    finally:
+        ft.ftblas_clear_fault_plan()
+        ft.ftblas_set_tile_policy("auto")
+
+
+@pytest.mark.parametrize("tB", ["N", "T"])
+def test_noft_pair_stress_matches_ft(tB):
+    """The non-FT pair-tile kernel (the same producer / cluster-free structure as the FT pair
+    kernel that once produced corrupted tiles) against the FT kernel at 2048^3, 5 repetitions:
+    bitwise equal to the FT output wherever no flip was planned (same mainloop and epilogue
+    formula), the planned elements within the bound of the FT (corrected) values, and every
+    repetition bitwise identical."""
+    import torch
+    ft = _lib("gemm", "pair")
+    try:
+        w = syn.Workload("t", 2048, 2048, 2048, "N", tB, 1.5, -0.5, "uniform", True, seed=9)
+        d = syn.make_inputs(w)
+        plan = syn.fault_plan(w.M, w.N, 100, 19)
+        C_ft, rep = run_gpu(ft, w, d, plan=plan)
+        assert rep.count == 100
+        mask = np.ones_like(C_ft, dtype=bool)
+        mask[plan[0], plan[1]] = False
+        ab = abs_product(w, d)[plan[0], plan[1]]
+        tol = gemm_bound(w.K, w.alpha, w.beta, ab, np.abs(d["C"][plan[0], plan[1]]))
+        first = None
+        for _ in range(5):
+            C_nf, _ = run_gpu(ft, w, d, noft=True)
+            assert np.array_equal(C_nf[mask], C_ft[mask])
+            assert (np.abs(C_nf[plan[0], plan[1]] - C_ft[plan[0], plan[1]]) <= tol).all()
+            if first is None:
+                first = C_nf
+            assert np.array_equal(C_nf, first)
+        sampled_check(w, d, first, n=200, seed=3)
+    finally:
+        ft.ftblas_clear_fault_plan()
+        ft.ftblas_set_tile_policy("auto")
+
+
 def test_host_entry_4x4_blocks_bitwise_equal_device():
     """The e2e entry at a size that takes the 4 x 4 block pipeline (16384^2 x 4096, beta != 0 so
     C0 blocks are uploaded too, 200 flips): C and the report equal the single device call's
