@@ -136,7 +136,12 @@ int ftblas_report_fetch(ftblas_err_report *err_report);
  * flips, flip k toggles bit bit[k] (0..63) of the accumulator of element
  * (i[k], j[k]) of C (0-based, 0 <= i < M, 0 <= j < N of the call) before the
  * epilogue.  Host arrays, copied.  n == 0 clears the plan.  Plans are matched
- * against the M x N of each call; entries outside it are ignored. */
+ * against the M x N of each call; entries outside it are ignored.  At most
+ * FTBLAS_MAX_FLIPS_PER_TILE flips may fall into one FTBLAS_TILE_M x FTBLAS_TILE_N
+ * tile (the persistent kernel keeps each thread's hits in registers); a plan
+ * with more returns -1 and leaves the installed plan unchanged.  Returns -1 for
+ * n < 0, -2 for NULL arrays or negative coordinates, -4 for a bit outside 0..63. */
+#define FTBLAS_MAX_FLIPS_PER_TILE 4
 int ftblas_set_fault_plan(int64_t n, const int64_t *i, const int64_t *j, const int32_t *bit);
 
 /* Where the checksum row/column of C (the border of C^f = A^c B^r, PAPER.md
@@ -157,11 +162,18 @@ int ftblas_get_checksum_mode(void);
 
 /* CTA tiling of the GEMM kernels (a performance choice; results, reports and the 128 x 128
  * verification tile are the same):
- *   FTBLAS_TILES_AUTO (default): FTBLAS_TILES_PAIR for K <= 2048, else FTBLAS_TILES_FULL;
+ *   FTBLAS_TILES_AUTO (default): for K <= 2048 FTBLAS_TILES_WS (ftblas_dgemm with at least
+ *       one tile per SM) or FTBLAS_TILES_PAIR (ftblas_dgemm_noft, fewer tiles), else
+ *       FTBLAS_TILES_FULL;
  *   FTBLAS_TILES_FULL: one CTA per 128 x 128 tile (8 MMA warps of 64 x 32, one CTA per SM);
  *   FTBLAS_TILES_PAIR: two CTAs per tile, each a 128 x 64 half (8 MMA warps of 32 x 32, two
  *       CTAs per SM so one CTA's epilogue overlaps another's mainloop); for ftblas_dgemm the halves form a
  *       thread-block cluster and exchange their row sums through distributed shared memory.
+ *   FTBLAS_TILES_WS: persistent kernel, one CTA per SM walking its tiles: 8 MMA warps
+ *       (TMA-fed DMMA mainloop; at the end of a tile they form out = alpha acc + beta C0 and
+ *       the checksum sums in registers, with C0 and out passed through tensor memory, and
+ *       verify the tile), 4 epilogue warps (C0 in, verified tile out, location) overlapping the
+ *       next tile's mainloop, 1 TMA producer thread.
  * The fused checksum mode always uses FTBLAS_TILES_FULL.  Returns 0, or -1 for an unknown
  * policy. */
 #define FTBLAS_TILES_AUTO 0

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <map>
 #include <vector>
 
 namespace {
@@ -249,31 +250,12 @@ bool make_operand_map(CUtensorMap *m, const double *X, long long ld, long long M
     return r == CUDA_SUCCESS;
 }
 
-// Tensor map of C for the persistent kernel's epilogue: dims {M, N}, box {128, 32}, no swizzle,
-// zero fill; false (the kernel then copies with plain L2-only accesses) if C is not 16-byte
-// aligned or ldc is odd.
-bool make_c_map(CUtensorMap *m, const double *C, long long ldc, long long M, long long N) {
-    std::memset(m, 0, sizeof(*m));
-    EncodeTiledFn fn = encode_tiled();
-    if (!fn || !C || M <= 0 || N <= 0 || (reinterpret_cast<uintptr_t>(C) & 15) || (ldc & 1)) return false;
-    if (M >= (1ll << 31) || N >= (1ll << 31)) return false;
-    const cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)N};
-    const cuuint64_t strides[1] = {(cuuint64_t)ldc * 8};
-    const cuuint32_t box[2] = {128u, (cuuint32_t)WS_QCOLS};
-    const cuuint32_t estr[2] = {1u, 1u};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(C), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 cudaError_t launch_ws_any(const void *kern, GemmArgs g, const CUtensorMap &ma, const CUtensorMap &mb, long long tiles,
                           cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_SMEM);
     if (e != cudaSuccess) return e;
-    CUtensorMap mc;
-    if (!make_c_map(&mc, g.C, g.ldc, g.M, g.N)) g.vecC = 0;
     const unsigned grid = (unsigned)std::min<long long>(tiles, sm_count());
-    void *args[] = {&g, const_cast<CUtensorMap *>(&ma), const_cast<CUtensorMap *>(&mb), &mc};
+    void *args[] = {&g, const_cast<CUtensorMap *>(&ma), const_cast<CUtensorMap *>(&mb)};
     e = cudaLaunchKernel(kern, dim3(grid), dim3(WS_THREADS), args, WS_SMEM, s);
     ctx().launches++;
     return e;
@@ -473,7 +455,15 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
     // the other) when the per-tile mainloop is short, 128 x 128 CTAs otherwise; the fused
     // checksum mode always uses 128 x 128
     const bool fused = ft && c.checksum_mode == FTBLAS_CHECKSUM_FUSED;
-    const bool ws = !fused && c.tile_policy == FTBLAS_TILES_WS;
+    // AUTO, FT calls with a short mainloop per tile (K <= pair_kmax): the persistent kernel, whose
+    // MMA warps do the epilogue arithmetic in registers and whose epilogue warps overlap C
+    // traffic and location with the next tile (c2: 4.47 ms vs 4.79 ms for pair tiles); non-FT
+    // calls there keep the pair tiles (4.02 vs 4.10 ms)
+    // (at least one wave of tiles: on a handful of tiles the persistent kernel's prologue is not
+    // amortized, c0 256^3: 0.42 vs 0.59 TFLOP/s)
+    const bool ws = !fused && (c.tile_policy == FTBLAS_TILES_WS ||
+                               (ft && c.tile_policy == FTBLAS_TILES_AUTO && K <= c.pair_kmax &&
+                                ntm * ntn >= sm_count()));
     const bool pair = !fused && !ws && (c.tile_policy == FTBLAS_TILES_PAIR ||
                                         (c.tile_policy == FTBLAS_TILES_AUTO && K <= c.pair_kmax));
     const Staging stg = make_staging(A, lda, M, kca, B, ldb, N, kcb, K, alpha, pair ? 64u : 128u);
@@ -899,8 +889,13 @@ int ftblas_set_fault_plan(int64_t n, const int64_t *i, const int64_t *j, const i
     Ctx &c = ctx();
     if (n < 0) return arg_fail(1, "n < 0");
     if (n > 0 && (!i || !j || !bit)) return arg_fail(2, "NULL plan array");
-    for (int64_t f = 0; f < n; f++)
+    std::map<std::pair<int64_t, int64_t>, int> per_tile;
+    for (int64_t f = 0; f < n; f++) {
         if (bit[f] < 0 || bit[f] > 63) return arg_fail(4, "bit out of [0,63]");
+        if (i[f] < 0 || j[f] < 0) return arg_fail(2, "negative plan coordinate");
+        if (++per_tile[{i[f] / FTBLAS_TILE_M, j[f] / FTBLAS_TILE_N}] > FTBLAS_MAX_FLIPS_PER_TILE)
+            return arg_fail(1, "more than FTBLAS_MAX_FLIPS_PER_TILE flips in one tile");
+    }
     c.plan_i.assign(i, i + n);
     c.plan_j.assign(j, j + n);
     c.plan_bit.assign(bit, bit + n);

@@ -79,6 +79,13 @@ def test_fault_plan_validation(lib):
     with pytest.raises(lib.FtblasError):
         lib.ftblas_set_fault_plan(np.array([1]), np.array([1]), np.array([64]))
     lib.ftblas_set_fault_plan(np.array([1, 2]), np.array([3, 4]), np.array([40, 62]))
+    # at most FTBLAS_MAX_FLIPS_PER_TILE (4) flips per 128 x 128 tile; 4 in one tile is fine
+    lib.ftblas_set_fault_plan(np.arange(4), np.arange(4), np.full(4, 50))
+    with pytest.raises(lib.FtblasError):
+        lib.ftblas_set_fault_plan(np.arange(5), np.arange(5), np.full(5, 50))
+    with pytest.raises(lib.FtblasError):
+        lib.ftblas_set_fault_plan(np.array([-1]), np.array([0]), np.array([50]))
+    lib.ftblas_set_fault_plan(np.array([0, 130, 260, 390, 520]), np.zeros(5, np.int64), np.full(5, 50))
     lib.ftblas_clear_fault_plan()
 
 

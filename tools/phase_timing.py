@@ -10,7 +10,7 @@ import numpy as np
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-L = ct.CDLL(os.path.join(ROOT, "tools", "exp", "phases.so"))
+L = ct.CDLL(os.path.join(ROOT, "tools", "var", "phases.so"))
 P, I, D = ct.c_void_p, ct.c_int64, ct.c_double
 common = [ct.c_char, ct.c_char, I, I, I, D, P, I, P, I, D, P, I]
 L.ftblas_dgemm.argtypes = common + [P]

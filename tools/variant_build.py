@@ -30,8 +30,9 @@ def build(name, kern, cu, extra=()):
         os.symlink(os.path.join(ROOT, "include"), os.path.join(base, "include"))
     open(os.path.join(d, "ftblas_kernels.cuh"), "w").write(kern)
     open(os.path.join(d, "ftblas.cu"), "w").write(cu)
-    os.makedirs(os.path.join(ROOT, "tools", "exp"), exist_ok=True)
-    out = os.path.join(ROOT, "tools", "exp", name + ".so")
+    open(os.path.join(d, "ftblas_ws.cuh"), "w").write(open(os.path.join(SRC, "ftblas_ws.cuh")).read())
+    os.makedirs(os.path.join(ROOT, "tools", "var"), exist_ok=True)
+    out = os.path.join(ROOT, "tools", "var", name + ".so")
     cmd = ["/usr/local/cuda/bin/nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
            "-lineinfo", "-Xcompiler", "-fPIC", "-shared", *extra, "-o", out, os.path.join(d, "ftblas.cu")]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -66,6 +67,44 @@ def phases():
     cu += ('\nextern "C" int ftblas_debug_times(void *dst) {\n'
            '    return (int)cudaMemcpyFromSymbol(dst, ftb::dbg_t, sizeof(unsigned long long) * 65536 * 8);\n}\n')
     return build("phases", k, cu)
+
+
+
+def loader_encode():
+    """Timing-only experiment: producer warps 1..3 of the 128 x 128 FT kernel
+    form e^T op(A) and op(B) e of every staged k-tile from shared memory (warp 1: the 32 column
+    sums of the A stage, warp 2: of the B stage, lane = k, 4 partial chains) as the paper's
+    packing-fused encoding would, consuming each stage like an MMA warp.  The sums go to a dummy
+    global so they are not eliminated; the regular encode pass still runs (results unchanged)."""
+    k, cu = read()
+    k = patch(k, "namespace ftb {\n", "namespace ftb {\n__device__ double dbg_loader_sink[1024];\n")
+    k = patch(k, "            mbar_init(&empty_bar[s], NT / 32);  // one arrival per MMA warp",
+              "            mbar_init(&empty_bar[s], NT / 32 + ((FT && NWN == 4) ? 2 : 0));")
+    k = patch(k, "            mbar_arrive(&norm_bar);\n        }\n",
+              "            mbar_arrive(&norm_bar);\n"
+              "            if (pt < 96) {\n"
+              "                const int wsel = (pt - 32) >> 5, kq = pt & 31;\n"
+              "                double acc4[4] = {0.0, 0.0, 0.0, 0.0};\n"
+              "                for (int kt = 0; kt < ktiles; kt++) {\n"
+              "                    const int st = kt % NS;\n"
+              "                    mbar_wait(&full_bar[st], (kt / NS) & 1);\n"
+              "                    const double *ts = wsel == 0 ? sA(st) : sB(st);\n"
+              "                    double s4[4] = {0.0, 0.0, 0.0, 0.0};\n"
+              "                    if (wsel == 0) {\n"
+              "#pragma unroll 8\n"
+              "                        for (int mn = 0; mn < 128; mn++) s4[mn & 3] += ts[Tile<KCA>::idx(mn, kq)];\n"
+              "                    } else {\n"
+              "#pragma unroll 8\n"
+              "                        for (int mn = 0; mn < BNT; mn++) s4[mn & 3] += ts[Tile<KCB, BNT>::idx(mn, kq)];\n"
+              "                    }\n"
+              "                    __syncwarp();\n"
+              "                    if ((pt & 31) == 0) mbar_arrive(&empty_bar[st]);\n"
+              "                    for (int u = 0; u < 4; u++) acc4[u] += s4[u];\n"
+              "                }\n"
+              "                dbg_loader_sink[(blockIdx.x * 64 + pt) & 1023] = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);\n"
+              "            }\n"
+              "        }\n")
+    return build("loader_encode", k, cu)
 
 
 if __name__ == "__main__":
