@@ -199,6 +199,9 @@ def main():
                          "path on fewer GPUs than ranks; not a performance configuration)")
     ap.add_argument("--tiles", default="auto", choices=["auto", "full", "pair", "ws"],
                     help="CTA tiling policy of the GEMM kernels (ftblas_set_tile_policy)")
+    ap.add_argument("--no-share-b-encoding", action="store_true",
+                    help="N > 1: every rank encodes all of op(B) (default: each rank encodes 1/N of its "
+                         "column tiles, all-gathered; shard.shared_b_encoding)")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-configs", action="store_true",
                     help="do not time BASELINE configs[0..2] beside the headline workload")
@@ -270,10 +273,35 @@ def main():
     flops_total = 2.0 * w.M * w.N * w.K
     flops_local = 2.0 * m * w.N * w.K
 
-    def gemm_ft(ta, tb, M_, N_, K_, al, A_, lda_, B_, ldb_, be, C_, ldc_, col_offset, append):
-        # blocks after the first reuse the checksum encoding of this rank's A (unchanged)
+    keep = []  # op(B) encodings of the current step (the kernels read them asynchronously)
+
+    def gemm_ft(ta, tb, M_, N_, K_, al, A_, lda_, B_, ldb_, be, C_, ldc_, col_offset, append, b_enc=None):
+        # blocks after the first reuse the checksum encoding of this rank's A (unchanged); with
+        # b_enc the block's op(B) encoding was computed once across the ranks (shard.shared_b_encoding)
+        if b_enc is not None:
+            b_enc = b_enc if b_enc.is_cuda else b_enc.cuda()
+            keep.append(b_enc)
+            fb.ftblas_set_b_encoding(b_enc, N_, K_)
         fb.ftblas_dgemm_ex(ta, tb, M_, N_, K_, al, A_, lda_, B_, ldb_, be, C_, ldc_, 0, col_offset, append,
-                           reuse_a=append)
+                           reuse_a=append, b_encoded=b_enc is not None)
+        if b_enc is not None:
+            fb.ftblas_set_b_encoding(None)
+
+    class Encoder:
+        """ftblas_encode_b for shard.shared_b_encoding; gloo collectives run on host copies."""
+        layout = staticmethod(fb.ftblas_b_encoding_layout)
+
+        @staticmethod
+        def empty(n):
+            return torch.empty(n, dtype=torch.float64, device="cuda" if args.backend == "nccl" else "cpu")
+
+        @staticmethod
+        def encode(tb, n, K_, B_, ldb_, out):
+            dst = out if out.is_cuda else torch.empty(out.numel(), dtype=torch.float64, device="cuda")
+            fb.ftblas_encode_b(tb, n, K_, B_, ldb_, dst)
+            if dst is not out:
+                out.copy_(dst)
+    encoder = Encoder() if (world > 1 and not args.no_share_b_encoding) else None
 
     def gemm_noft(ta, tb, M_, N_, K_, al, A_, lda_, B_, ldb_, be, C_, ldc_, col_offset, append):
         fb.ftblas_dgemm_noft(ta, tb, M_, N_, K_, al, A_, lda_, B_, ldb_, be, C_, ldc_)
@@ -287,9 +315,11 @@ def main():
 
     def step(gemm, broadcast):
         # C := alpha AB + beta C accumulates into C; the value drifts but the work is identical
+        keep.clear()
         shard.sharded_dgemm(gemm, w.transA, w.transB, w.M, w.N, w.K, w.alpha, A_dev, lda, B_dev,
                             d["ldb"], w.beta, C_dev, ldc, rank=rank, world=world,
-                            broadcast=broadcast and world > 1, chunks=chunks if broadcast else 1)
+                            broadcast=broadcast and world > 1, chunks=chunks if broadcast else 1,
+                            encoder=encoder if gemm is gemm_ft else None)
 
     def timed(fn, steps, warm=1):
         for _ in range(warm):  # first launches of a kernel instantiation load its module
@@ -498,6 +528,8 @@ def main():
                            (f", op(B) {args.backend.upper()} broadcast per step in {len(chunks)} column chunks "
                             f"{[c1 - c0 for c0, c1 in chunks]} overlapped with the GEMM"
                             if isinstance(chunks, list) else f", op(B) {args.backend.upper()} broadcast per step")
+                           + (f"; op(B) encoding shared: each rank encodes 1/{world} of each chunk's column tiles, "
+                              "all-gathered" if encoder is not None else "; op(B) encoded on every rank")
                            if world > 1 else ""),
                        l2="no flush: operands (%.1f GiB) >> 126 MB L2" % ((d["A"].nbytes + d["B"].nbytes + d["C"].nbytes) / 2**30)),
             "fp64_peak_tflops": FP64_PEAK_TFLOPS,

@@ -99,13 +99,38 @@ int ftblas_dgemm(char transA, char transB, int64_t M, int64_t N, int64_t K, doub
  * it (clear it with ftblas_report_reset); FTBLAS_REUSE_A_ENCODE -- the caller guarantees that
  * op(A) (same pointer, lda, M, K, transA) is unchanged since the previous FT call, whose A
  * checksum encoding is then reused if still cached (column blocks of one product); other
- * bits -> -16. */
+ * FTBLAS_B_ENCODED -- see ftblas_set_b_encoding; other bits -> -16. */
 #define FTBLAS_REPORT_APPEND 1
 #define FTBLAS_REUSE_A_ENCODE 2
+#define FTBLAS_B_ENCODED 4 /* op(B)'s encoding comes from ftblas_set_b_encoding (see below) */
 int ftblas_dgemm_ex(char transA, char transB, int64_t M, int64_t N, int64_t K, double alpha,
                     const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
                     double *C, int64_t ldc, int64_t row_offset, int64_t col_offset, int32_t flags,
                     ftblas_err_report *err_report);
+
+/* Shared op(B) encoding (sharded products: the B-side encoding -- w_J = op(B) e_J of every
+ * column tile J, the column 1-norms and the tile maxima of reading R4 --
+ * depends on op(B) only, so the ranks of a row-sharded product can each encode a slice of the
+ * column tiles and exchange the slices instead of every rank encoding all of op(B); PAPER.md
+ * section V.B: the packed B is shared and its checksum reduced once).
+ *   ftblas_b_encoding_layout: the encoding of an op(B) with N columns and inner dimension K is
+ *     *total doubles: [0, *off_nrm) the ceil(N/128) vectors w_J of Kp = max(32, ceil(K/32) 32)
+ *     doubles each (zero for k >= K), [*off_nrm, *off_nrm + N) the column norms,
+ *     [*off_max, *off_max + ceil(N/128)) the tile maxima.  Columns [c0, c1) of whole tiles of an
+ *     encoding are the encoding of those columns, section by section.  Returns 0, -1 / -2 for
+ *     N / K < 0.  ftblas_b_encoding_len returns *total (or -1).
+ *   ftblas_encode_b: op(B) (K x N; B, ldb as for ftblas_dgemm; device pointers) -> enc (caller-
+ *     owned device buffer of ftblas_b_encoding_len(N, K) doubles), stream-ordered on the library
+ *     stream.  Returns 0; -1 transB, -2 N < 0, -3 K < 0, -4 B NULL, -5 ldb, -6 enc NULL;
+ *     FTBLAS_ERR_CUDA.
+ *   ftblas_set_b_encoding: install enc (an encoding of an N x K op(B); NULL uninstalls) for
+ *     ftblas_dgemm_ex calls with FTBLAS_B_ENCODED, which use it in place of encoding their op(B)
+ *     (their N and K must match, else -16).  The caller keeps enc alive and unchanged while such
+ *     calls are in flight. */
+int64_t ftblas_b_encoding_len(int64_t N, int64_t K);
+int ftblas_b_encoding_layout(int64_t N, int64_t K, int64_t *off_nrm, int64_t *off_max, int64_t *total);
+int ftblas_encode_b(char transB, int64_t N, int64_t K, const double *B, int64_t ldb, double *enc);
+int ftblas_set_b_encoding(const double *enc, int64_t N, int64_t K);
 
 /* Clear the device report (stream-ordered; for FTBLAS_REPORT_APPEND sequences). */
 int ftblas_report_reset(void);

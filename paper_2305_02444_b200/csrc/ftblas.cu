@@ -45,6 +45,9 @@ struct Ctx {
     DevBuf rep;           // ReportHdr + entries
     long long rep_cap = 1 << 16;
     DevBuf pend;          // PendingHdr + correction candidates of the persistent kernel
+    DevBuf encws;         // ftblas_encode_b: per-k-chunk norm partials
+    const double *b_enc = nullptr;  // ftblas_set_b_encoding (used by FTBLAS_B_ENCODED calls)
+    long long b_enc_N = -1, b_enc_K = -1;
     long long pend_cap = 1 << 16;
     DevBuf plan_dev;      // fault plan: i, j (caller coordinates), bit, CSR offsets by caller tile
     long long plan_version = 0, plan_uploaded = -1;
@@ -428,10 +431,21 @@ cudaError_t cksum_gemm(bool kcx, const double *X, long long ldx, long long P, co
     return cudaErrorInvalidValue;
 }
 
+// Layout of a finalized op(B) encoding (ftblas_encode_b; doubles, sections 16-byte aligned):
+// [0, oN): WB, ceil(N/128) rows of Kp (w_J = op(B) e_J, zero for k >= K); [oN, oN + N): the
+// column 1-norms ||op(B)(:, j)||_1; [oM, oM + ceil(N/128)): the tile maxima max_k sum_j |op(B)(k, j)|.
+void b_layout(long long N, long long K, long long &oN, long long &oM, long long &total) {
+    const long long Kp = std::max<long long>(BK, (K + BK - 1) / BK * BK), ntn = (N + BN - 1) / BN;
+    auto al = [](long long n) { return (n + 1) / 2 * 2; };
+    oN = al(ntn * Kp);
+    oM = oN + al(N);
+    total = oM + al(ntn);
+}
+
 int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K, double alpha,
                const double *A, long long lda, const double *B, long long ldb, double beta, double *C,
                long long ldc, ftblas_err_report *rep, long long off_i = 0, long long off_j = 0,
-               bool append = false, bool reuse_a = false, bool inject = true) {
+               bool append = false, bool reuse_a = false, bool inject = true, const double *benc = nullptr) {
     static_assert(sizeof(Correction) == sizeof(ftblas_correction), "ABI");
     Ctx &c = ctx();
     int rc = check_args(ta, tb, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta);
@@ -521,8 +535,20 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
         double *lineA = w + oLA, *tmaxA = w + oTA;
         g.WB = w + oWB;
         double *lineB = w + oLB, *tmaxB = w + oTB;
+        // FTBLAS_B_ENCODED: op(B)'s finalized encoding (ftblas_encode_b, e.g. assembled from the
+        // slices that the ranks of a sharded product encoded) replaces the B side of the encode pass
+        const bool ext_b = benc != nullptr && K > 0 && alpha != 0.0;
+        int kchB = kch;
+        if (ext_b) {
+            long long oN, oM, tot;
+            b_layout(N, K, oN, oM, tot);
+            g.WB = benc;
+            lineB = const_cast<double *>(benc) + oN;
+            tmaxB = const_cast<double *>(benc) + oM;
+            kchB = 1;
+        }
         g.lineA = lineA; g.lineB = lineB; g.tmaxA = tmaxA; g.tmaxB = tmaxB;
-        g.kch = kch; g.Kp = Kp;
+        g.kch = kch; g.kchB = kchB; g.Kp = Kp;
         double *Rpre = w + oR, *Spre = w + oS;
         double *fin = w + oF;
         g.fin_nrmA = fin; g.fin_nrmB = fin + M; g.fin_maxA = fin + M + N; g.fin_maxB = fin + M + N + ntm;
@@ -549,15 +575,19 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
         EncodeArgs ea{};
         const EncodeOperand opA{A, lda, M, kca ? 1 : 0, va ? 1 : 0, const_cast<double *>(g.VA), lineA, tmaxA, (int)ntm};
         const EncodeOperand opB{B, ldb, N, kcb ? 1 : 0, vb ? 1 : 0, const_cast<double *>(g.WB), lineB, tmaxB, (int)ntn};
-        ea.op[0] = skip_a ? opB : opA;
-        ea.op[1] = opB;
+        int nops = 0;
+        if (!skip_a) ea.op[nops++] = opA;
+        if (!ext_b) ea.op[nops++] = opB;
         ea.K = (alpha == 0.0) ? 0 : K;  // alpha == 0: A, B are not read (encodes are zero)
         ea.Kp = Kp; ea.kper = kper; ea.kch = kch; ea.rep = append ? nullptr : g.rep;
         ea.pend = g.pend;
         // one launch per layout path (encode_kernel<PATH>): both operands in one launch when
         // they share it; the first launch zeroes the report
         {
-            const int nops = skip_a ? 1 : 2;
+            if (nops == 0) {  // nothing to encode: the report and candidate list are cleared here
+                if (!append) CK(cudaMemsetAsync(g.rep, 0, sizeof(ReportHdr), c.stream), "report reset");
+                CK(cudaMemsetAsync(g.pend, 0, sizeof(PendingHdr), c.stream), "pending reset");
+            }
             auto path_of = [](const EncodeOperand &o) { return o.kc ? 0 : (o.vec ? 1 : 2); };
             ReportHdr *rep0 = ea.rep;
             for (int b0 = 0; b0 < nops;) {
@@ -611,7 +641,7 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
             fa.lineA = lineA; fa.lineB = lineB; fa.tmaxA = tmaxA; fa.tmaxB = tmaxB;
             fa.Rp = rs_final ? nullptr : Rpre; fa.Sp = rs_final ? nullptr : Spre;  // nullptr: nothing to sum
             fa.M = M; fa.N = N; fa.ntm = ntm; fa.ntn = ntn; fa.stride_r = g.stride_r; fa.stride_s = g.stride_s;
-            fa.kch = kch; fa.splits_r = (int)spR; fa.splits_s = (int)spS;
+            fa.kch = kch; fa.kchB = kchB; fa.splits_r = (int)spR; fa.splits_s = (int)spS;
             fa.nrmA = fin; fa.nrmB = fin + M; fa.maxA = fin + M + N; fa.maxB = fin + M + N + ntm;
             fa.R = fin + M + N + ntm + ntn; fa.S = fa.R + (size_t)ntn * M;
             const long long total = (long long)(M + N + ntm + ntn) + (rs_final ? 0 : (long long)ntn * M + (long long)ntm * N);
@@ -677,9 +707,88 @@ int ftblas_dgemm_ex(char transA, char transB, int64_t M, int64_t N, int64_t K, d
                     int64_t row_offset, int64_t col_offset, int32_t flags, ftblas_err_report *err_report) {
     if (row_offset < 0 || row_offset % FTBLAS_TILE_M) return arg_fail(14, "row_offset not a multiple of the tile");
     if (col_offset < 0 || col_offset % FTBLAS_TILE_N) return arg_fail(15, "col_offset not a multiple of the tile");
-    if (flags & ~(FTBLAS_REPORT_APPEND | FTBLAS_REUSE_A_ENCODE)) return arg_fail(16, "unknown flags");
+    if (flags & ~(FTBLAS_REPORT_APPEND | FTBLAS_REUSE_A_ENCODE | FTBLAS_B_ENCODED)) return arg_fail(16, "unknown flags");
+    const double *benc = nullptr;
+    if (flags & FTBLAS_B_ENCODED) {
+        const Ctx &c = ctx();
+        if (!c.b_enc || c.b_enc_N != N || c.b_enc_K != K)
+            return arg_fail(16, "FTBLAS_B_ENCODED without a matching ftblas_set_b_encoding");
+        benc = c.b_enc;
+    }
     return dgemm_impl(true, transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, err_report, row_offset,
-                      col_offset, (flags & FTBLAS_REPORT_APPEND) != 0, (flags & FTBLAS_REUSE_A_ENCODE) != 0);
+                      col_offset, (flags & FTBLAS_REPORT_APPEND) != 0, (flags & FTBLAS_REUSE_A_ENCODE) != 0, true,
+                      benc);
+}
+
+int64_t ftblas_b_encoding_len(int64_t N, int64_t K) {
+    if (N < 0 || K < 0) return -1;
+    long long oN, oM, total;
+    b_layout(N, K, oN, oM, total);
+    return total;
+}
+
+int ftblas_b_encoding_layout(int64_t N, int64_t K, int64_t *off_nrm, int64_t *off_max, int64_t *total) {
+    if (N < 0) return arg_fail(1, "N < 0");
+    if (K < 0) return arg_fail(2, "K < 0");
+    long long oN, oM, t;
+    b_layout(N, K, oN, oM, t);
+    if (off_nrm) *off_nrm = oN;
+    if (off_max) *off_max = oM;
+    if (total) *total = t;
+    return 0;
+}
+
+int ftblas_encode_b(char transB, int64_t N, int64_t K, const double *B, int64_t ldb, double *enc) {
+    Ctx &c = ctx();
+    if (!trans_ok(transB)) return arg_fail(1, "transB");
+    if (N < 0) return arg_fail(2, "N < 0");
+    if (K < 0) return arg_fail(3, "K < 0");
+    const bool kcb = !is_t(transB);
+    if (ldb < std::max<long long>(1, is_t(transB) ? N : K)) return arg_fail(5, "ldb too small");
+    if (N > 0 && K > 0 && !B) return arg_fail(4, "B is NULL");
+    if (N > 0 && !enc) return arg_fail(6, "enc is NULL");
+    if (N == 0) return 0;
+    long long oN, oM, total;
+    b_layout(N, K, oN, oM, total);
+    if (K == 0) {  // empty inner dimension: every sum is zero
+        CK(cudaMemsetAsync(enc, 0, (size_t)total * sizeof(double), c.stream), "encoding zero");
+        return 0;
+    }
+    const long long Kp = std::max<long long>(BK, (K + BK - 1) / BK * BK), ntn = (N + BN - 1) / BN;
+    long long kch_l = (8 * 2 * 148 + ntn - 1) / ntn;
+    const int kch = (int)std::max<long long>(1, std::min<long long>({kch_l, 32, std::max<long long>(1, Kp / 128)}));
+    const long long kper = ((Kp + kch - 1) / kch + 31) / 32 * 32;
+    // per-k-chunk partials of the norms, summed into the encoding by side_finalize_kernel
+    const size_t nl = ((size_t)kch * N + 1) / 2 * 2, nt = ((size_t)kch * ntn + 1) / 2 * 2;
+    CK(c.encws.ensure((nl + nt) * sizeof(double)), "cudaMalloc(encode workspace)");
+    double *line = c.encws.as<double>(), *tmax = line + nl;
+    EncodeArgs ea{};
+    ea.op[0] = EncodeOperand{B, ldb, N, kcb ? 1 : 0, vec_ok(B, ldb) ? 1 : 0, enc, line, tmax, (int)ntn};
+    ea.K = K; ea.Kp = Kp; ea.kper = kper; ea.kch = kch; ea.rep = nullptr; ea.pend = nullptr; ea.op_base = 0;
+    const dim3 grid((unsigned)ntn, (unsigned)kch, 1u);
+    const int path = ea.op[0].kc ? 0 : (ea.op[0].vec ? 1 : 2);
+    if (path == 0) encode_kernel<0><<<grid, NTHREADS, 0, c.stream>>>(ea);
+    else if (path == 1) encode_kernel<1><<<grid, NTHREADS, 0, c.stream>>>(ea);
+    else encode_kernel<2><<<grid, NTHREADS, 0, c.stream>>>(ea);
+    c.launches++;
+    CK(cudaGetLastError(), "encode_kernel launch");
+    FinArgs fa{};
+    fa.lineB = line; fa.tmaxB = tmax; fa.N = N; fa.ntn = ntn; fa.kch = kch; fa.kchB = kch;
+    fa.nrmB = enc + oN; fa.maxB = enc + oM;
+    const unsigned blocks = (unsigned)std::min<long long>((N + ntn + 255) / 256, 8 * 148);
+    side_finalize_kernel<<<blocks, 256, 0, c.stream>>>(fa);
+    c.launches++;
+    CK(cudaGetLastError(), "side_finalize_kernel launch");
+    return 0;
+}
+
+int ftblas_set_b_encoding(const double *enc, int64_t N, int64_t K) {
+    Ctx &c = ctx();
+    if (enc && (N < 0 || K < 0)) return arg_fail(2, "N or K < 0");
+    c.b_enc = enc;
+    c.b_enc_N = enc ? N : -1;
+    c.b_enc_K = enc ? K : -1;
+    return 0;
 }
 
 int ftblas_report_reset(void) {
@@ -982,6 +1091,7 @@ int ftblas_release(void) {
     Ctx &c = ctx();
     cudaStreamSynchronize(c.stream);
     c.ws.release(); c.ws_gen++; c.a_valid = false; c.rep.release(); c.pend.release(); c.plan_dev.release();
+    c.encws.release();
     c.plan_uploaded = -1;
     c.hA.release(); c.hB.release(); c.hC.release();
     return 0;

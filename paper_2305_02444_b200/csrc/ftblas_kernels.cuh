@@ -142,7 +142,7 @@ struct GemmArgs {
     const double *lineB;   // kch x N : partial sum_k |op(B)(k,j)|
     const double *tmaxA;   // kch x ntm: partial max_k sum_i |op(A)(i,k)|
     const double *tmaxB;   // kch x ntn
-    int kch;
+    int kch, kchB;         // partial counts of the A side / the B side (1: finalized, ftblas_encode_b)
     long long Kp;
     const double *Rpre;    // FT_PRE: [splits_r][ntn][M], R[tn][i] = sum_k op(A)(i,k) WB[tn][k] (k-split partials)
     const double *Spre;    // FT_PRE: [splits_s][ntm][N], S[tm][j] = sum_k VA[tm][k] op(B)(k,j)
@@ -714,13 +714,13 @@ __global__ void __launch_bounds__(Warps<NWN>::NT + Warps<NWN>::PT, NWN == 2 ? 2 
                 } else if (q < 128 + BNT) {
                     const long long gj = n0 + (q - 128);
                     const bool ok = gj < g.N;
-                    nrm_col[q - 128] = !ok ? 0.0 : sum_strided(g.lineB + gj, g.N, g.kch);
+                    nrm_col[q - 128] = !ok ? 0.0 : sum_strided(g.lineB + gj, g.N, g.kchB);
                     if (MODE == MODE_FT_PRE)
                         pre_s[q - 128] = !ok ? 0.0 : sum_strided(g.Spre + tm * g.N + gj, g.stride_s, g.splits_s);
                 } else if (q == 128 + BNT) {
                     nrm_max[0] = max_strided(g.tmaxA + tm, ntm, g.kch);
                 } else {
-                    nrm_max[1] = max_strided(g.tmaxB + tn, ntn, g.kch);
+                    nrm_max[1] = max_strided(g.tmaxB + tn, ntn, g.kchB);
                 }
             }
             mbar_arrive(&norm_bar);
@@ -1197,7 +1197,7 @@ __global__ void __launch_bounds__(Warps<NWN>::NT + Warps<NWN>::PT, NWN == 2 ? 2 
 struct FinArgs {
     const double *lineA, *lineB, *tmaxA, *tmaxB, *Rp, *Sp;
     long long M, N, ntm, ntn, stride_r, stride_s;
-    int kch, splits_r, splits_s;
+    int kch, kchB, splits_r, splits_s;
     double *nrmA, *nrmB, *maxA, *maxB, *R, *S;
 };
 __global__ void __launch_bounds__(256) side_finalize_kernel(FinArgs f) {
@@ -1208,11 +1208,11 @@ __global__ void __launch_bounds__(256) side_finalize_kernel(FinArgs f) {
         long long y = x;
         if (y < nA) { f.nrmA[y] = sum_strided(f.lineA + y, f.M, f.kch); continue; }
         y -= nA;
-        if (y < nB) { f.nrmB[y] = sum_strided(f.lineB + y, f.N, f.kch); continue; }
+        if (y < nB) { f.nrmB[y] = sum_strided(f.lineB + y, f.N, f.kchB); continue; }
         y -= nB;
         if (y < nmA) { f.maxA[y] = max_strided(f.tmaxA + y, f.ntm, f.kch); continue; }
         y -= nmA;
-        if (y < nmB) { f.maxB[y] = max_strided(f.tmaxB + y, f.ntn, f.kch); continue; }
+        if (y < nmB) { f.maxB[y] = max_strided(f.tmaxB + y, f.ntn, f.kchB); continue; }
         y -= nmB;
         if (y < nR) { f.R[y] = sum_strided(f.Rp + y, f.stride_r, f.splits_r); continue; }
         y -= nR;

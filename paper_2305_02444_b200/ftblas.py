@@ -78,6 +78,14 @@ def _load():
     L.ftblas_set_checksum_mode.restype = ct.c_int
     L.ftblas_get_checksum_mode.argtypes = []
     L.ftblas_get_checksum_mode.restype = ct.c_int
+    L.ftblas_b_encoding_len.argtypes = [I, I]
+    L.ftblas_b_encoding_len.restype = I
+    L.ftblas_b_encoding_layout.argtypes = [I, I, ct.POINTER(I), ct.POINTER(I), ct.POINTER(I)]
+    L.ftblas_b_encoding_layout.restype = ct.c_int
+    L.ftblas_encode_b.argtypes = [ct.c_char, I, I, P, I, P]
+    L.ftblas_encode_b.restype = ct.c_int
+    L.ftblas_set_b_encoding.argtypes = [P, I, I]
+    L.ftblas_set_b_encoding.restype = ct.c_int
     return L
 
 
@@ -89,12 +97,14 @@ EXPORTS = ("ftblas_dgemm", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_rep
            "ftblas_tile_shape", "ftblas_last_error", "ftblas_release", "ftblas_profile",
            "ftblas_profile_read", "ftblas_set_checksum_mode", "ftblas_get_checksum_mode",
            "ftblas_dgemm_ex", "ftblas_report_reset", "ftblas_set_tile_policy",
-           "ftblas_get_tile_policy")
+           "ftblas_get_tile_policy", "ftblas_b_encoding_len", "ftblas_b_encoding_layout",
+           "ftblas_encode_b", "ftblas_set_b_encoding")
 
 TILES = {"auto": 0, "full": 1, "pair": 2, "ws": 3}  # FTBLAS_TILES_*
 
 REPORT_APPEND = 1  # FTBLAS_REPORT_APPEND
 REUSE_A_ENCODE = 2  # FTBLAS_REUSE_A_ENCODE
+B_ENCODED = 4  # FTBLAS_B_ENCODED
 
 CHECKSUM_GEMM = 0   # FTBLAS_CHECKSUM_GEMM: checksum row/column by two DMMA GEMMs (default)
 CHECKSUM_FUSED = 1  # FTBLAS_CHECKSUM_FUSED: accumulated in the main GEMM's mainloop
@@ -162,12 +172,32 @@ def ftblas_dgemm(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, r
 
 
 def ftblas_dgemm_ex(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, row_offset=0,
-                    col_offset=0, append=False, report=None, reuse_a=False):
+                    col_offset=0, append=False, report=None, reuse_a=False, b_encoded=False):
     rep = ct.byref(report.c) if report is not None else None
-    flags = (REPORT_APPEND if append else 0) | (REUSE_A_ENCODE if reuse_a else 0)
+    flags = (REPORT_APPEND if append else 0) | (REUSE_A_ENCODE if reuse_a else 0) | \
+        (B_ENCODED if b_encoded else 0)
     _check(lib.ftblas_dgemm_ex(_tc(transA), _tc(transB), M, N, K, alpha, _ptr(A), lda, _ptr(B), ldb,
                                beta, _ptr(C), ldc, row_offset, col_offset, flags, rep))
     return report
+
+
+def ftblas_b_encoding_layout(N, K):
+    """(off_nrm, off_max, total) in doubles of the op(B) encoding layout (include/ftblas.h)."""
+    a, b, t = ct.c_int64(), ct.c_int64(), ct.c_int64()
+    _check(lib.ftblas_b_encoding_layout(N, K, ct.byref(a), ct.byref(b), ct.byref(t)))
+    return a.value, b.value, t.value
+
+
+def ftblas_b_encoding_len(N, K) -> int:
+    return lib.ftblas_b_encoding_len(N, K)
+
+
+def ftblas_encode_b(transB, N, K, B, ldb, enc):
+    _check(lib.ftblas_encode_b(_tc(transB), N, K, _ptr(B), ldb, _ptr(enc)))
+
+
+def ftblas_set_b_encoding(enc, N=0, K=0):
+    _check(lib.ftblas_set_b_encoding(_ptr(enc), N, K))
 
 
 def ftblas_report_reset():

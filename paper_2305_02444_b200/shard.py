@@ -88,9 +88,60 @@ def broadcast_chunk_bounds(m: int, N: int, sms: int = 148, waves=(1, 2, 4)) -> l
     return out
 
 
+def b_encoding_slices(n: int, world: int) -> list:
+    """Per rank, the column tiles [t0, t1) of an n-column op(B) it encodes, and its column count."""
+    ntn = -(-n // TILE_N)
+    out = []
+    for r in range(world):
+        t0, t1 = shard_rows(ntn, world, r, align=1)
+        out.append((t0, t1, max(0, min(n, t1 * TILE_N) - t0 * TILE_N)))
+    return out
+
+
+def assemble_b_encoding(pieces, n: int, K: int, layout, out):
+    """The encoding of an n-column op(B) (``layout(n, K)`` = (off_nrm, off_max, total), the
+    library's section layout) assembled in ``out`` from the per-rank encodings ``pieces[r]`` of
+    the column tiles ``b_encoding_slices(n, len(pieces))[r]``: section by section (the w_J rows,
+    the column norms, the tile maxima), a copy only -- every value is tile- or column-local."""
+    kp = layout(TILE_N, K)[0]  # one tile: the w_J section is exactly Kp doubles
+    o_n, o_m, _ = layout(n, K)
+    for (t0, t1, nr), piece in zip(b_encoding_slices(n, len(pieces)), pieces):
+        if nr == 0:
+            continue
+        p_n, p_m, _ = layout(nr, K)
+        out[t0 * kp: t1 * kp] = piece[: (t1 - t0) * kp]
+        out[o_n + t0 * TILE_N: o_n + t0 * TILE_N + nr] = piece[p_n: p_n + nr]
+        out[o_m + t0: o_m + t1] = piece[p_m: p_m + (t1 - t0)]
+    return out
+
+
+def shared_b_encoding(encoder, transB, n: int, K: int, B, ldb: int, *, rank: int, world: int,
+                      group=None):
+    """op(B)'s encoding (n columns; B: flat column-major storage of this op(B)'s columns, a torch
+    tensor) computed once across the ranks: rank r encodes its slice of the column tiles
+    (``encoder.encode(transB, nr, K, B_slice, ldb, piece)``, ftblas_encode_b in production) and
+    the slices are all-gathered (one collective) and assembled section by section on every rank.
+    ``encoder.layout(n, K)`` is the library's layout (ftblas_b_encoding_layout) and
+    ``encoder.empty(len)`` allocates a float64 tensor where the collective runs."""
+    import torch.distributed as dist
+    slices = b_encoding_slices(n, world)
+    lmax = max(encoder.layout(nr, K)[2] if nr else 0 for _, _, nr in slices) or 1
+    t0, _, nr = slices[rank]
+    piece = encoder.empty(lmax)
+    piece.zero_()
+    if nr:
+        c0 = t0 * TILE_N
+        view = B[c0 * ldb:] if transB in ("N", "n") else B[c0:]
+        encoder.encode(transB, nr, K, view, ldb, piece)
+    gathered = encoder.empty(world * lmax)
+    dist.all_gather_into_tensor(gathered, piece, group=group)
+    pieces = [gathered[r * lmax:(r + 1) * lmax] for r in range(world)]
+    return assemble_b_encoding(pieces, n, K, encoder.layout, encoder.empty(encoder.layout(n, K)[2]))
+
+
 def sharded_dgemm(gemm, transA, transB, M, N, K, alpha, A_shard, lda, B, ldb, beta, C_shard, ldc,
                   *, rank: int, world: int, src: int = 0, group=None, broadcast: bool = True,
-                  chunks=1):
+                  chunks=1, encoder=None):
     """One sharded step on this rank.
 
     ``gemm(transA, transB, m, n, K, alpha, A, lda, B, ldb, beta, C, ldc, col_offset, append)``
@@ -107,8 +158,17 @@ def sharded_dgemm(gemm, transA, transB, M, N, K, alpha, A_shard, lda, B, ldb, be
     transB = 'N' (column blocks of op(B) are contiguous in B) it is split into column blocks
     of whole tiles, all posted asynchronously on the communication stream; the GEMM of block
     c waits only for block c, so the broadcast of the later blocks overlaps the DMMA work of
-    the earlier ones.  Returns this rank's rows range.
+    the earlier ones.  With an ``encoder`` (see ``shared_b_encoding``) each block's op(B)
+    encoding is computed once across the ranks and passed to ``gemm`` as ``b_enc`` (else every
+    rank encodes all of op(B) inside its GEMM calls).  Returns this rank's rows range.
     """
+    def run(q, n, b_view, c_view, c0, append):
+        kw = {}
+        if encoder is not None and multi:
+            kw["b_enc"] = shared_b_encoding(encoder, transB, n, K, b_view, ldb, rank=rank, world=world,
+                                            group=group)
+        gemm(transA, transB, m, n, K, alpha, A_shard, lda, b_view, ldb, beta, c_view, ldc, c0, append, **kw)
+
     r0, r1 = shard_rows(M, world, rank)
     m = r1 - r0
     multi = broadcast and world > 1
@@ -120,15 +180,14 @@ def sharded_dgemm(gemm, transA, transB, M, N, K, alpha, A_shard, lda, B, ldb, be
         for q, (c0, c1) in enumerate(bounds):
             if rank != src:
                 works[q].wait()  # NCCL: the compute stream waits for block q, the host does not
-            gemm(transA, transB, m, c1 - c0, K, alpha, A_shard, lda, B[c0 * ldb:], ldb, beta,
-                 C_shard[c0 * ldc:], ldc, c0, q > 0)
+            run(q, c1 - c0, B[c0 * ldb:], C_shard[c0 * ldc:], c0, q > 0)
         if rank == src:
             for w in works:
                 w.wait()
         return r0, r1
     if multi:
         broadcast_b(B, src, group)
-    gemm(transA, transB, m, N, K, alpha, A_shard, lda, B, ldb, beta, C_shard, ldc, 0, False)
+    run(0, N, B, C_shard, 0, False)
     return r0, r1
 
 

@@ -89,6 +89,20 @@ def test_fault_plan_validation(lib):
     lib.ftblas_clear_fault_plan()
 
 
+def test_b_encoding_host_checks(lib):
+    """FTBLAS_B_ENCODED needs a matching installed encoding (checked before any CUDA work); the
+    layout of an N x K encoding: ceil(N/128) rows of Kp, then N norms, then the tile maxima."""
+    import numpy as np
+    with pytest.raises(lib.FtblasError):
+        lib.ftblas_dgemm_ex("N", "N", 4, 4, 4, 1.0, 1, 4, 1, 4, 0.0, 1, 4, b_encoded=True)
+    off_n, off_m, tot = lib.ftblas_b_encoding_layout(300, 90)
+    assert (off_n, off_m, tot) == (3 * 96, 3 * 96 + 300, 3 * 96 + 300 + 4)
+    assert lib.ftblas_b_encoding_len(300, 90) == tot and lib.ftblas_b_encoding_layout(128, 1)[0] == 32
+    with pytest.raises(lib.FtblasError):
+        lib.ftblas_encode_b("X", 4, 4, 1, 4, 1)
+    lib.ftblas_set_b_encoding(None)
+
+
 def test_product_has_no_oracle_or_cpu_fallback():
     """The product package never imports the oracle and has no CPU compute path."""
     pkg = os.path.join(ROOT, "paper_2305_02444_b200")

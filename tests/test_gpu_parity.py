@@ -282,6 +282,47 @@ def test_blocked_calls_growing_workspace(ft):
     assert_close(w, d, C, C_ref)
 
 
+@pytest.mark.parametrize("tB", ["N", "T"])
+def test_shared_b_encoding(ft, tB):
+    """op(B)'s encoding computed in column slices (ftblas_encode_b, as the
+    ranks of a sharded product do), assembled by shard.assemble_b_encoding and passed with
+    FTBLAS_B_ENCODED: reports and C equal the oracle's, in two column blocks (the second reusing
+    the A encoding), under every tiling."""
+    import torch
+    from paper_2305_02444_b200 import shard
+    w = syn.Workload("benc", 300, 700, 90, "N", tB, 1.5, -0.5, "uniform", True, seed=41)
+    d = syn.make_inputs(w)
+    plan = syn.fault_plan(w.M, w.N, 5, 23)
+    A_t, pA = to_dev(d["A"]); B_t, pB = to_dev(d["B"]); C_t, pC = to_dev(d["C"])
+    ft.ftblas_set_fault_plan(*plan)
+    ft.ftblas_report_reset()
+    ldb = d["ldb"]
+    for q, (c0, c1) in enumerate([(0, 256), (256, 700)]):
+        n = c1 - c0
+        b_off = c0 * ldb if tB == "N" else c0
+        pieces = []
+        for t0, t1, nr in shard.b_encoding_slices(n, 3):
+            piece = torch.zeros(max(1, ft.ftblas_b_encoding_len(nr, w.K)), dtype=torch.float64, device="cuda")
+            if nr:
+                off = b_off + (t0 * 128 * ldb if tB == "N" else t0 * 128)
+                ft.ftblas_encode_b(tB, nr, w.K, pB + 8 * off, ldb, piece)
+            pieces.append(piece)
+        enc = torch.zeros(ft.ftblas_b_encoding_len(n, w.K), dtype=torch.float64, device="cuda")
+        shard.assemble_b_encoding(pieces, n, w.K, ft.ftblas_b_encoding_layout, enc)
+        ft.ftblas_set_b_encoding(enc, n, w.K)
+        ft.ftblas_dgemm_ex("N", tB, w.M, n, w.K, w.alpha, pA, d["lda"], pB + 8 * b_off, ldb, w.beta,
+                           pC + 8 * c0 * d["ldc"], d["ldc"], 0, c0, q > 0, reuse_a=q > 0, b_encoded=True)
+        torch.cuda.synchronize()
+        ft.ftblas_set_b_encoding(None)
+    rep = ft.ftblas_report_fetch(ft.Report(64))
+    ft.ftblas_clear_fault_plan()
+    C = from_dev(C_t, d["C"])
+    C_ref, orep, st = run_oracle(w, d, plan)
+    assert rep.count == st.count == 5 and rep.tiles_flagged == st.tiles_flagged
+    assert report_key(rep.entries()) == report_key(orep)
+    assert_close(w, d, C, C_ref)
+
+
 def _flip(x: float, bit: int) -> float:
     import struct
     b = struct.unpack("<Q", struct.pack("<d", x))[0] ^ (1 << bit)

@@ -138,3 +138,88 @@ def test_broadcast_chunk_bounds_geometric_whole_waves():
         assert sum(waves) <= math.ceil(ideal) + 1, (m, N, b, waves, ideal)
     # c3 at 8 GPUs: 9 / 18 / 37 tile-columns (1, 2, 4 waves), then the rest
     assert [(c1 - c0) // 128 for c0, c1 in shard.broadcast_chunk_bounds(2048, 16384)] == [9, 18, 37, 64]
+
+
+class _NumpyEncoder:
+    """Test stand-in for ftblas_encode_b on CPU tensors: the definitions of the B-side encoding
+    (w_J = sum of the tile's columns, column 1-norms, tile maxima of the row |.| sums) written into
+    the library's section layout (ftblas_b_encoding_layout, which needs no GPU)."""
+
+    def __init__(self):
+        from paper_2305_02444_b200 import ftblas
+        self.layout = ftblas.ftblas_b_encoding_layout
+
+    def empty(self, n):
+        return torch.empty(n, dtype=torch.float64)
+
+    def encode(self, transB, n, K, B, ldb, out):
+        Bv = B.numpy()
+        if transB in ("N", "n"):
+            P = np.stack([Bv[j * ldb: j * ldb + K] for j in range(n)], axis=1)          # K x n
+        else:
+            P = np.stack([Bv[k * ldb: k * ldb + n] for k in range(K)], axis=0)          # K x n
+        o_n, o_m, tot = self.layout(n, K)
+        kp = self.layout(128, K)[0]
+        e = np.zeros(tot)
+        for t in range(-(-n // 128)):
+            blk = P[:, t * 128:(t + 1) * 128]
+            e[t * kp: t * kp + K] = blk.sum(axis=1)
+            e[o_m + t] = np.abs(blk).sum(axis=1).max() if K else 0.0
+        e[o_n: o_n + n] = np.abs(P).sum(axis=0)
+        out[:tot] = torch.from_numpy(e)
+
+
+def _enc_worker(rank, world, port, tB, chunks, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        M, N, K = 256, 700, 70
+        rng = np.random.default_rng(5)
+        Bm = rng.uniform(-1, 1, (K, N) if tB == "N" else (N, K))
+        ldb = Bm.shape[0]
+        B_t = torch.from_numpy(np.asfortranarray(Bm).reshape(-1, order="F").copy()) if rank == 0 \
+            else torch.zeros(Bm.size, dtype=torch.float64)
+        enc = _NumpyEncoder()
+        seen = []
+
+        def gemm(ta, tb, m, n, K_, al, A_, lda_, B_, ldb_, be, C_, ldc_, col_offset, append, b_enc=None):
+            ref = enc.empty(enc.layout(n, K_)[2])
+            enc.encode(tb, n, K_, B_, ldb_, ref)
+            seen.append((col_offset, n, bool(torch.equal(b_enc, ref))))
+
+        A = np.zeros((M, K))
+        C = torch.zeros(M * N, dtype=torch.float64)
+        shard.sharded_dgemm(gemm, "N", tB, M, N, K, 1.0, A, M, B_t, ldb, 0.0, C, M, rank=rank, world=world,
+                            chunks=chunks, encoder=enc)
+        q.put((rank, seen))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("tB,chunks", [("N", 1), ("N", 3), ("T", 1)])
+def test_shared_b_encoding_equals_whole_encoding(tB, chunks):
+    """Every rank's assembled op(B) encoding (slices encoded by the ranks, all-gathered) equals the
+    encoding of the whole block, for every column block of the chunked broadcast."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_enc_worker, args=(r, world, port, tB, chunks, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, seen in res:
+        assert seen and all(ok for _, _, ok in seen), seen
+        assert sum(n for _, n, _ in seen) == 700
+
+
+def test_b_encoding_slices_cover_tiles():
+    for n in (1, 128, 300, 700, 16384):
+        for world in (1, 2, 3, 8):
+            sl = shard.b_encoding_slices(n, world)
+            assert sl[0][0] == 0 and sl[-1][1] == -(-n // 128)
+            assert sum(nr for _, _, nr in sl) == n
+            assert all(a[1] == b[0] for a, b in zip(sl, sl[1:]))
