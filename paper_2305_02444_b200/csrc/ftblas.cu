@@ -442,6 +442,13 @@ void b_layout(long long N, long long K, long long &oN, long long &oM, long long 
     total = oM + al(ntn);
 }
 
+cudaError_t launch_encode(int p0, int p1, dim3 grid, const EncodeArgs &ea, cudaStream_t s) {
+#define L(x, y) if (p0 == x && p1 == y) { encode_kernel<x, y><<<grid, NTHREADS, 0, s>>>(ea); return cudaGetLastError(); }
+    L(0, 0) L(0, 1) L(0, 2) L(1, 0) L(1, 1) L(1, 2) L(2, 0) L(2, 1) L(2, 2)
+#undef L
+    return cudaErrorInvalidValue;
+}
+
 int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K, double alpha,
                const double *A, long long lda, const double *B, long long ldb, double beta, double *C,
                long long ldc, ftblas_err_report *rep, long long off_i = 0, long long off_j = 0,
@@ -581,32 +588,23 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
         ea.K = (alpha == 0.0) ? 0 : K;  // alpha == 0: A, B are not read (encodes are zero)
         ea.Kp = Kp; ea.kper = kper; ea.kch = kch; ea.rep = append ? nullptr : g.rep;
         ea.pend = g.pend;
-        // one launch per layout path (encode_kernel<PATH>): both operands in one launch when
-        // they share it; the first launch zeroes the report
+        // one launch (encode_kernel<PATH0, PATH1>: operand z along its own layout path), which
+        // also zeroes the report (unless appending) and the candidate list
         {
             if (nops == 0) {  // nothing to encode: the report and candidate list are cleared here
                 if (!append) CK(cudaMemsetAsync(g.rep, 0, sizeof(ReportHdr), c.stream), "report reset");
                 CK(cudaMemsetAsync(g.pend, 0, sizeof(PendingHdr), c.stream), "pending reset");
             }
             auto path_of = [](const EncodeOperand &o) { return o.kc ? 0 : (o.vec ? 1 : 2); };
-            ReportHdr *rep0 = ea.rep;
-            for (int b0 = 0; b0 < nops;) {
-                int b1 = b0 + 1;
-                while (b1 < nops && path_of(ea.op[b1]) == path_of(ea.op[b0])) b1++;
+            if (nops > 0) {
+                // one launch for both operands (blockIdx.z), each along its own layout path
                 long long tiles = 0;
-                for (int q = b0; q < b1; q++) tiles = std::max<long long>(tiles, ea.op[q].ntiles);
-                ea.op_base = b0;
-                ea.rep = b0 == 0 ? rep0 : nullptr;
-                ea.pend = b0 == 0 ? g.pend : nullptr;
-                const dim3 grid((unsigned)tiles, (unsigned)kch, (unsigned)(b1 - b0));
-                switch (path_of(ea.op[b0])) {
-                    case 0: encode_kernel<0><<<grid, NTHREADS, 0, c.stream>>>(ea); break;
-                    case 1: encode_kernel<1><<<grid, NTHREADS, 0, c.stream>>>(ea); break;
-                    default: encode_kernel<2><<<grid, NTHREADS, 0, c.stream>>>(ea); break;
-                }
+                for (int q = 0; q < nops; q++) tiles = std::max<long long>(tiles, ea.op[q].ntiles);
+                ea.op_base = 0;
+                const dim3 grid((unsigned)tiles, (unsigned)kch, (unsigned)nops);
+                const int p0 = path_of(ea.op[0]), p1 = path_of(ea.op[nops - 1]);
+                CK(launch_encode(p0, p1, grid, ea, c.stream), "encode_kernel launch");
                 c.launches++;
-                CK(cudaGetLastError(), "encode_kernel launch");
-                b0 = b1;
             }
         }
         if (!skip_a) {
@@ -634,9 +632,10 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
             CK(cudaMemsetAsync(Rpre, 0, (oS - oR + (size_t)spS * ntm * N) * sizeof(double), c.stream), "checksum zero");
             (void)nRS;
         }
-        if (pre && (pair || ws)) {
+        if (pre && pair) {
             // per-row / per-column side data of the verification: partials summed once (the
-            // pair-tile producers copy them; 128 x 128 tiles sum the partials in the producer)
+            // pair-tile producers copy them; 128 x 128 tiles sum the partials in the producer, the
+            // persistent kernel's epilogue warps as they load a tile's C0)
             FinArgs fa{};
             fa.lineA = lineA; fa.lineB = lineB; fa.tmaxA = tmaxA; fa.tmaxB = tmaxB;
             fa.Rp = rs_final ? nullptr : Rpre; fa.Sp = rs_final ? nullptr : Spre;  // nullptr: nothing to sum
@@ -767,11 +766,8 @@ int ftblas_encode_b(char transB, int64_t N, int64_t K, const double *B, int64_t 
     ea.K = K; ea.Kp = Kp; ea.kper = kper; ea.kch = kch; ea.rep = nullptr; ea.pend = nullptr; ea.op_base = 0;
     const dim3 grid((unsigned)ntn, (unsigned)kch, 1u);
     const int path = ea.op[0].kc ? 0 : (ea.op[0].vec ? 1 : 2);
-    if (path == 0) encode_kernel<0><<<grid, NTHREADS, 0, c.stream>>>(ea);
-    else if (path == 1) encode_kernel<1><<<grid, NTHREADS, 0, c.stream>>>(ea);
-    else encode_kernel<2><<<grid, NTHREADS, 0, c.stream>>>(ea);
+    CK(launch_encode(path, path, grid, ea, c.stream), "encode_kernel launch");
     c.launches++;
-    CK(cudaGetLastError(), "encode_kernel launch");
     FinArgs fa{};
     fa.lineB = line; fa.tmaxB = tmax; fa.N = N; fa.ntn = ntn; fa.kch = kch; fa.kchB = kch;
     fa.nrmB = enc + oN; fa.maxB = enc + oM;

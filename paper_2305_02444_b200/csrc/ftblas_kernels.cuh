@@ -472,9 +472,9 @@ __device__ void encode_k_contig(const EncodeOperand &o, const EncodeArgs &a, int
 
 // PATH 0: k contiguous (slab walk, cross-warp k sums in shared memory);
 // PATH 1 / 2: mn contiguous with 16-byte / 8-byte loads.  3 blocks / SM (<= 80 registers): a
-// latency-bound stream that wants loads in flight).  Operand = a.op[a.op_base + blockIdx.z];
-// the host launches once per layout path (once in total when both operands share it).
-template <int PATH>
+// latency-bound stream that wants loads in flight).  Operand = a.op[a.op_base + blockIdx.z],
+// laid out along PATH0 (z = 0) or PATH1 (z = 1): both operands in one launch.
+template <int PATH0, int PATH1>
 __global__ void __launch_bounds__(NTHREADS, 3) encode_kernel(EncodeArgs a) {
     __shared__ double red[(NTHREADS / 32) * 128];
     __shared__ double wmax[NTHREADS / 32];
@@ -488,8 +488,9 @@ __global__ void __launch_bounds__(NTHREADS, 3) encode_kernel(EncodeArgs a) {
     const long long kbeg = (long long)ch * a.kper;
     const long long kend = min(kbeg + a.kper, a.Kp);
     double tm = 0.0;
-    if (PATH == 0)      encode_k_contig(o, a, t, kbeg, kend, red, tm);
-    else if (PATH == 1) encode_mn_contig<true>(o, a, t, kbeg, kend, red, tm);
+    const int path = blockIdx.z == 0 ? PATH0 : PATH1;  // block-uniform
+    if (path == 0)      encode_k_contig(o, a, t, kbeg, kend, red, tm);
+    else if (path == 1) encode_mn_contig<true>(o, a, t, kbeg, kend, red, tm);
     else                encode_mn_contig<false>(o, a, t, kbeg, kend, red, tm);
 #pragma unroll
     for (int off = 16; off; off >>= 1) tm = fmax(tm, __shfl_xor_sync(0xffffffffu, tm, off));

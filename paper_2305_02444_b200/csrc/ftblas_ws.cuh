@@ -64,6 +64,12 @@ __device__ __forceinline__ int ws_mma_idx(int w) {  // 0..7 over the two MMA war
     return 4 * (wg - below) + (w & 3);
 }
 constexpr int WS_TMEM_WARP = 4 * WS_PROD_WG + 1;  // allocates / frees TMEM (not the TMA thread's warp)
+#ifndef FTB_WS_C0_PREFETCH  // the producer prefetches into L2 the C0 of the tile this many ahead (0: none)
+#define FTB_WS_C0_PREFETCH 1
+#endif
+#ifndef FTB_WSX_NOMAX  // timing experiments only: 1 = skip the |C0| column maxima in the epilogue
+#define FTB_WSX_NOMAX 0
+#endif
 #ifndef FTB_WS_STAGES
 #define FTB_WS_STAGES 3
 #endif
@@ -99,7 +105,7 @@ __device__ __forceinline__ unsigned long long ws_now() {
 #define WS_T(v)
 #define WS_ADD(slot, t0)
 #endif
-enum { WP_MMA_WAIT_FULL = 0, WP_MMA_WAIT_BUF, WP_MMA_TAIL, WP_EPI_WAIT_ACC, WP_EPI_C0LOAD, WP_EPI_SIDE,
+enum { WP_MMA_WAIT_FULL = 0, WP_MMA_WAIT_BUF, WP_MMA_TAIL, WP_EPI_WAIT_ACC, WP_EPI_C0LOAD, WP_MMA_KLOOP,
        WP_EPI_VERIFY, WP_EPI_LOCATE, WP_EPI_STORE, WP_PROD_WAIT_EMPTY, WP_EPI_TOTAL, WP_MMA_TOTAL };
 
 // ------------------------------------------------------------------ primitives
@@ -139,6 +145,31 @@ __device__ __forceinline__ int ld_ro(const int *p) {
     int v;
     asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];\n" : "=r"(v) : "l"(p));
     return v;
+}
+
+// sum / max of p[c * stride], c < n, in index order (as side_finalize_kernel), L1-bypassing loads
+__device__ __forceinline__ double sum_strided_ro(const double *p, long long stride, int n) {
+    double s = 0.0;
+    for (int c0 = 0; c0 < n; c0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) v[u] = (c0 + u < n) ? ld_ro(p + (long long)(c0 + u) * stride) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+            if (c0 + u < n) s += v[u];
+    }
+    return s;
+}
+__device__ __forceinline__ double max_strided_ro(const double *p, long long stride, int n) {
+    double m = 0.0;
+    for (int c0 = 0; c0 < n; c0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) v[u] = (c0 + u < n) ? ld_ro(p + (long long)(c0 + u) * stride) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; u++) m = fmax(m, v[u]);
+    }
+    return m;
 }
 
 // Fragment view of TMEM (MMA warps), 16x256b shape, 2 repetitions: repetition r carries
@@ -293,6 +324,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     // they load C0, per row (the row's thread) and per column (per epilogue warp)
     __shared__ unsigned redm_r[RB][FT ? BM : 1], redm_c[RB][FT ? 4 : 1][FT ? BN : 1];
     __shared__ int rflag[FT ? BM : 1], cflag[FT ? BN : 1];
+#ifdef FTB_WSX_PADSMEM  // timing experiment only: static shared memory of the FT kernel in the non-FT one
+    __shared__ double wsx_pad[FT ? 1 : 2816];
+    if (threadIdx.x == 0) wsx_pad[blockIdx.x % 2816] = 0.0;
+#endif
     double *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) / 8u;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long ntm = (g.M + BM - 1) / BM, ntn = (g.N + BN - 1) / BN, ntiles = ntm * ntn;
@@ -335,11 +370,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 long long tm, tn;
                 tile_coords(x, ntm, ntn, tm, tn);
                 const long long m0 = tm * BM, n0 = tn * BN;
-                if (pt == 0 && need_c0 && x + 2 * (long long)gridDim.x < ntiles) {
-                    // C0 of the tile after next -> L2: the epilogue loads it into TMEM while this
-                    // tile's mainloop runs
+                if (FTB_WS_C0_PREFETCH && pt == 0 && need_c0 && x + FTB_WS_C0_PREFETCH * (long long)gridDim.x < ntiles) {
+                    // C0 of the next tile (FTB_WS_C0_PREFETCH tiles ahead) -> L2: the epilogue loads
+                    // it into TMEM after storing the tile before this one, ~20 us later
                     long long tm2, tn2;
-                    tile_coords(x + 2 * (long long)gridDim.x, ntm, ntn, tm2, tn2);
+                    tile_coords(x + FTB_WS_C0_PREFETCH * (long long)gridDim.x, ntm, ntn, tm2, tn2);
                     const unsigned bytes = (unsigned)(min((long long)BM, g.M - tm2 * BM) * 8) & ~15u;
                     const long long nv = min((long long)BN, g.N - tn2 * BN);
                     if (bytes && g.vecC)
@@ -390,13 +425,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 const long long mvalid = min((long long)BM, g.M - m0), nvalid = min((long long)BN, g.N - n0);
                 const long long gi = m0 + et, gj = n0 + et;
                 WsSide &sd = side[buf & (RB - 1)];
-                sd.nrm_row[et] = et < mvalid ? ld_ro(g.fin_nrmA + gi) : 0.0;
-                sd.pre_r[et] = et < mvalid ? ld_ro(g.fin_R + tn * g.M + gi) : 0.0;
-                sd.nrm_col[et] = et < nvalid ? ld_ro(g.fin_nrmB + gj) : 0.0;
-                sd.pre_s[et] = et < nvalid ? ld_ro(g.fin_S + tm * g.N + gj) : 0.0;
+                // the encode pass's per-k-chunk partials and the checksum GEMMs' k-split partials,
+                // summed here in index order (no side_finalize_kernel launch on this path)
+                sd.nrm_row[et] = et < mvalid ? sum_strided_ro(g.lineA + gi, g.M, g.kch) : 0.0;
+                sd.pre_r[et] = et < mvalid ? sum_strided_ro(g.Rpre + tn * g.M + gi, g.stride_r, g.splits_r) : 0.0;
+                sd.nrm_col[et] = et < nvalid ? sum_strided_ro(g.lineB + gj, g.N, g.kchB) : 0.0;
+                sd.pre_s[et] = et < nvalid ? sum_strided_ro(g.Spre + tm * g.N + gj, g.stride_s, g.splits_s) : 0.0;
                 if (et == 0) {
-                    sd.nrm_max[0] = ld_ro(g.fin_maxA + tm);
-                    sd.nrm_max[1] = ld_ro(g.fin_maxB + tn);
+                    sd.nrm_max[0] = max_strided_ro(g.tmaxA + tm, ntm, g.kch);
+                    sd.nrm_max[1] = max_strided_ro(g.tmaxB + tn, ntn, g.kchB);
                     flags[buf & (RB - 1)][0] = 0;
                     flags[buf & (RB - 1)][1] = 0;
                 }
@@ -418,7 +455,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                     }
 #pragma unroll
                 for (int u = 0; u < 2; u++) tmem_st8d(tb + ((c + u) >> 3) * 128 + 16 * ((c + u) & 7), v[u]);
-                if (FT) {  // |C0| maxima: the row in-thread, each column over the warp's 32 rows
+                if (FT && !FTB_WSX_NOMAX) {  // |C0| maxima: the row in-thread, each column over the warp's 32 rows
 #pragma unroll
                     for (int u = 0; u < 2; u++)
 #pragma unroll
@@ -743,6 +780,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             unsigned phase = 0;
             for (long long x = blockIdx.x; x < ntiles; x += gridDim.x, it++) {
                 zero_acc();
+                WS_T(tk0);
 #pragma unroll 1
                 for (int kt = 0; kt < ktiles; kt++) {
                     WS_T(tf0);
@@ -766,11 +804,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                     }
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty_bar[st]);
+                    if (kt == 0 && mw == 0 && lane == 0) WS_ADD(WP_EPI_VERIFY, tk0);  // first k-tile
                     if (++st == WS_STAGES) {
                         st = 0;
                         phase ^= 1u;
                     }
                 }
+                if (mw == 0 && lane == 0) WS_ADD(WP_MMA_KLOOP, tk0);
                 finish(x, it);
             }
             if (mw == 0 && lane == 0) WS_ADD(WP_MMA_TOTAL, tm0);

@@ -8,7 +8,7 @@ import numpy as np, torch
 import synthetic as syn
 from tests._util import to_dev
 from paper_2305_02444_b200 import ftblas as ft
-names = ["mma_wait_full", "mma_wait_buf", "mma_tail", "epi_wait_acc", "epi_c0load", "epi_side", "epi_verify",
+names = ["mma_wait_full", "mma_wait_buf", "mma_tail", "epi_wait_acc", "epi_c0load", "mma_kloop", "epi_verify",
          "epi_locate", "epi_store", "prod_wait_empty", "epi_total", "mma_total"]
 w = syn.CONFIG_BY_NAME[sys.argv[1]]
 mode = sys.argv[2] if len(sys.argv) > 2 else "ft"
