@@ -804,7 +804,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                     }
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty_bar[st]);
-                    if (kt == 0 && mw == 0 && lane == 0) WS_ADD(WP_EPI_VERIFY, tk0);  // first k-tile
                     if (++st == WS_STAGES) {
                         st = 0;
                         phase ^= 1u;

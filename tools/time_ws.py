@@ -7,6 +7,9 @@ import synthetic as syn
 from tests._util import to_dev
 from paper_2305_02444_b200 import ftblas as ft
 w = syn.CONFIG_BY_NAME[sys.argv[1]]
+if os.environ.get("BETA") is not None:  # override beta (development: the C0 traffic's share)
+    import dataclasses
+    w = dataclasses.replace(w, beta=float(os.environ["BETA"]))
 tiles = sys.argv[2] if len(sys.argv) > 2 else "ws"
 d = syn.make_inputs(w)
 ft.ftblas_set_stream(torch.cuda.current_stream()); ft.ftblas_set_tile_policy(tiles)
