@@ -8,20 +8,23 @@
 //             mbarrier ring that runs across tile boundaries, and prefetches the C0 of the
 //             CTA's next tile into L2 when it starts a tile;
 //   MMA       (8 warps, 32 x 64 warp tiles: MMA warp w owns rows 32 (w % 4) .. +31, columns
-//             64 (w / 4) .. +63): DMMA into registers.  At the end of a tile the accumulators get
-//             the planned flips (test harness), and the MMA warps themselves form, in registers,
-//             out = alpha acc + beta C0 with C0 read from TMEM (written there by the epilogue
-//             warps during the mainloop) and -- FT -- the row / column partial sums of
-//             d = out - beta C0 and the |C0| maxima (readings R3, R4k); out goes back into the
-//             same TMEM positions, the partials to shared memory, and the warps start the next
-//             tile.  The FP64 epilogue arithmetic thus runs in the warps that own the FP64 pipe,
-//             for about 1 us per tile, instead of beside their DMMA stream (where an FP64
-//             instruction of another warp waits ~75 cycles for an issue slot,
-//             tools/fp64_side.cu);
-//   epilogue  (4 warps, one TMEM lane = one tile row per thread): verify every row and column
-//             against the checksum-GEMM references, locate (lines 540, 521;
-//             readings R5-R7: candidates listed for correct_kernel), store the verified tile
-//             from TMEM to C, and load the C0 of the tile after next into the freed TMEM buffer.
+//             64 (w / 4) .. +63): DMMA into registers.  At the end of a tile (the "tail") the
+//             accumulators get the planned flips (test harness), and the MMA warps themselves
+//             form, in registers, out = alpha acc + beta C0 with C0 read from TMEM (written there
+//             by the epilogue warps during the mainloop) and -- FT -- the row / column partial
+//             sums of d = out - beta C0 (reading R3); out goes back into the same TMEM
+//             positions, the partials to shared memory, and after a barrier each MMA thread
+//             verifies one row or column of the tile against the checksum-GEMM references
+//             (readings R4, R4k) and lists it if flagged; then the warps start
+//             the next tile.  The FP64 epilogue arithmetic thus runs in the warps that own the
+//             FP64 pipe, about 1.8 us per tile (FT) while no warp issues DMMAs, instead of beside
+//             the DMMA stream (where an FP64 instruction of another warp waits ~75 cycles for an
+//             issue slot, tools/fp64_side.cu);
+//   epilogue  (4 warps, one TMEM lane = one tile row per thread): locate (lines 540, 521;
+//             readings R5-R7: candidates of flagged rows x columns listed for correct_kernel),
+//             store the verified tile from TMEM to C, and load the C0 (with its |C0| row / column
+//             maxima, integer pipe) and the verification references of the tile after next into
+//             the freed TMEM buffer / shared memory.
 // TMEM: 2 buffers x 256 columns x 128 lanes x 32 bit = all 512 columns, lane = tile row.  MMA
 // warp w reads / writes with the 16x256b shape (a thread of fragment row g owns lanes g and
 // g + 8: the mma.sync accumulator layout), so fragments a = 2p, 2p + 1 sit in lanes
