@@ -162,6 +162,25 @@ def test_multiple_errors_in_one_tile(ft):
     assert_close(w, d, C_gpu, C_ref)
 
 
+def test_four_flips_in_one_tile_same_thread(ft):
+    """FTBLAS_MAX_FLIPS_PER_TILE (4) flips in one tile, three of them on elements one thread of
+    the persistent kernel holds (same row, adjacent columns; the row below), plus a lone flip in
+    another tile: every flip is applied (the per-thread hit list and its jump table), reports
+    bit-exact vs the oracle (candidate path, kind 2), C within the tolerance."""
+    w = syn.Workload("t", 256, 256, 96, "N", "N", 1.25, 0.5, "uniform", True, seed=8)
+    d = syn.make_inputs(w)
+    # (3, 8), (3, 10), (1, 8): fragment rows a = 1, 0 of row group g = 1 and columns (t = 0, e = 0 /
+    # 1) of fragment column b = 1 -- one thread of MMA warp 0 in the 32 x 64 warp tiling
+    plan = (np.array([3, 3, 1, 70, 200], np.int64), np.array([8, 10, 8, 100, 140], np.int64),
+            np.array([53, 57, 61, 49, 55], np.int32))
+    C_gpu, rep = run_gpu(ft, w, d, plan=plan)
+    C_ref, orep, st = run_oracle(w, d, plan)
+    assert report_key(rep.entries()) == report_key(orep)
+    assert rep.count == st.count
+    assert sorted((e["i"], e["j"]) for e in rep.entries()) == [(1, 8), (3, 8), (3, 10), (70, 100), (200, 140)]
+    assert_close(w, d, C_gpu, C_ref)
+
+
 @pytest.mark.parametrize("bit", [40, 47, 51, 52, 55, 60, 61, 62])
 def test_each_bit_class(ft, bit):
     w = syn.Workload("t", 256, 256, 200, "N", "N", 1.0, 0.0, "normal", False, seed=bit)
