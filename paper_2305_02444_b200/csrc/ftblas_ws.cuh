@@ -83,7 +83,12 @@ constexpr int WS_SMEM = WS_STAGES * WS_STAGE_EL * 8 + 1024;
 // setmaxnreg split of the 64 K registers (one CTA per SM): the MMA warps hold 128 accumulator
 // registers plus the epilogue chunk and partial sums at the end of a tile
 struct WsRegs {
-    static constexpr int MMA = 200, EPI = 80, PROD = 32;
+#ifndef FTB_WS_REG_MMA  // (overridable for experiments)
+#define FTB_WS_REG_MMA 200
+#define FTB_WS_REG_EPI 80
+#define FTB_WS_REG_PROD 32
+#endif
+    static constexpr int MMA = FTB_WS_REG_MMA, EPI = FTB_WS_REG_EPI, PROD = FTB_WS_REG_PROD;
     static_assert(256 * MMA + 128 * EPI + 128 * PROD <= 65536,
                   "setmaxnreg budget exceeds the register file of one CTA per SM");
 };
