@@ -332,6 +332,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     // they load C0, per row (the row's thread) and per column (per epilogue warp)
     __shared__ unsigned redm_r[RB][FT ? BM : 1], redm_c[RB][FT ? 4 : 1][FT ? BN : 1];
     __shared__ int rflag[FT ? BM : 1], cflag[FT ? BN : 1];
+    // FT, per TMEM buffer: the fault plan's CSR range of its tile (test harness), looked up by the
+    // epilogue warps with the references so that no dependent global load sits in the tile tail
+    __shared__ int plan_rng[RB][2];
 #ifdef FTB_WSX_PADSMEM  // timing experiment only: static shared memory of the FT kernel in the non-FT one
     __shared__ double wsx_pad[FT ? 1 : 2816];
     if (threadIdx.x == 0) wsx_pad[blockIdx.x % 2816] = 0.0;
@@ -444,6 +447,19 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                     sd.nrm_max[1] = max_strided_ro(g.tmaxB + tn, ntn, g.kchB);
                     flags[buf & (RB - 1)][0] = 0;
                     flags[buf & (RB - 1)][1] = 0;
+                }
+                if (et == 32) {  // planned flips of the tile: [lo, hi) of the plan's CSR (empty without a plan)
+                    int lo = 0, hi = 0;
+                    if (g.plan_ptr) {
+                        const long long gtm = tm + g.off_i / BM, gtn = tn + g.off_j / BN;
+                        if (gtm < g.plan_ntm && gtn < g.plan_ntn) {
+                            const long long tix = gtn * g.plan_ntm + gtm;
+                            lo = ld_ro(g.plan_ptr + tix);
+                            hi = ld_ro(g.plan_ptr + tix + 1);
+                        }
+                    }
+                    plan_rng[buf & (RB - 1)][0] = lo;
+                    plan_rng[buf & (RB - 1)][1] = hi;
                 }
             }
             if (!need_c0) return;
@@ -620,15 +636,24 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             constexpr int BMODE = decltype(bm_c)::value;  // 0: beta = 0, 1: beta = 1, 2: other
             long long tm, tn;
             tile_coords(x, ntm, ntn, tm, tn);
-            // planned flips of this tile (test harness): each thread collects the hits on its own
+            const int buf = it & 1, rb = buf & (RB - 1);
+            WS_T(te0);
+            // all MMA warps leave the DMMA stream together and enter the next tile together: an
+            // FP64 instruction issued beside another warp's DMMA stream waits ~75 cycles for the
+            // pipe (tools/fp64_side.cu)
+            mma_bar();
+            ws_wait(&buf_ready[buf], (unsigned)((it >> 1) & 1));
+            tc_fence_after();
+            // planned flips of this tile (test harness; after the buffer wait: plan_rng is the
+            // epilogue's): each thread collects the hits on its own
             // 64 elements (index k = 16 a + 2 b + e; at most FTBLAS_MAX_FLIPS_PER_TILE = 4 per
             // tile, checked by ftblas_set_fault_plan), then flips each through a jump table
             int hk[4] = {-1, -1, -1, -1}, hb[4] = {0, 0, 0, 0};
-            if (FT && g.plan_ptr) {
-                const long long gtm = tm + g.off_i / BM, gtn = tn + g.off_j / BN;
-                if (gtm < g.plan_ntm && gtn < g.plan_ntn) {
-                    const long long tix = gtn * g.plan_ntm + gtm;
-                    const int lo = ld_ro(g.plan_ptr + tix), hi = ld_ro(g.plan_ptr + tix + 1);
+            if (FT) {
+                // [lo, hi) of the plan's CSR, looked up by the epilogue warps with the tile's
+                // references (prep): no dependent global load in the tail of a clean tile
+                const int lo = plan_rng[rb][0], hi = plan_rng[rb][1];
+                {
                     for (int f = lo; f < hi; f++) {
                         const long long li = ld_ro(g.plan_i + f) - g.off_i - tm * BM;
                         const long long lj = ld_ro(g.plan_j + f) - g.off_j - tn * BN;
@@ -661,14 +686,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                         default: break;
                     }
                 }
-            const int buf = it & 1, rb = buf & (RB - 1);
-            WS_T(te0);
-            // all MMA warps leave the DMMA stream together and enter the next tile together: an
-            // FP64 instruction issued beside another warp's DMMA stream waits ~75 cycles for the
-            // pipe (tools/fp64_side.cu)
-            mma_bar();
-            ws_wait(&buf_ready[buf], (unsigned)((it >> 1) & 1));
-            tc_fence_after();
             if (mw == 0 && lane == 0) WS_ADD(WP_MMA_WAIT_BUF, te0);
             WS_T(ts0);
             const long long mvalid = min((long long)BM, g.M - tm * BM), nvalid = min((long long)BN, g.N - tn * BN);
