@@ -632,10 +632,12 @@ int dgemm_impl(bool ft, char ta, char tb, long long M, long long N, long long K,
             CK(cudaMemsetAsync(Rpre, 0, (oS - oR + (size_t)spS * ntm * N) * sizeof(double), c.stream), "checksum zero");
             (void)nRS;
         }
-        if (pre && pair) {
+        if (pre && (pair || ws)) {
             // per-row / per-column side data of the verification: partials summed once (the
-            // pair-tile producers copy them; 128 x 128 tiles sum the partials in the producer, the
-            // persistent kernel's epilogue warps as they load a tile's C0)
+            // pair-tile producers and the persistent kernel's epilogue warps copy them: an FP64
+            // add issued by an epilogue warp beside the DMMA stream waits ~1000 cycles for the
+            // pipe, 32 of them per tile made the epilogue warps the bottleneck at K = 256;
+            // 128 x 128 tiles sum the partials in the producer)
             FinArgs fa{};
             fa.lineA = lineA; fa.lineB = lineB; fa.tmaxA = tmaxA; fa.tmaxB = tmaxB;
             fa.Rp = rs_final ? nullptr : Rpre; fa.Sp = rs_final ? nullptr : Spre;  // nullptr: nothing to sum

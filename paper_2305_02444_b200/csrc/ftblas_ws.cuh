@@ -73,6 +73,9 @@ constexpr int WS_TMEM_WARP = 4 * WS_PROD_WG + 1;  // allocates / frees TMEM (not
 #ifndef FTB_WSX_NOMAX  // timing experiments only: 1 = skip the |C0| column maxima in the epilogue
 #define FTB_WSX_NOMAX 0
 #endif
+#ifndef FTB_WSX_NOSIDE  // timing experiments only: 1 = skip the verification references' partial sums in prep
+#define FTB_WSX_NOSIDE 0
+#endif
 #ifndef FTB_WS_STAGES
 #define FTB_WS_STAGES 3
 #endif
@@ -432,19 +435,30 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             long long tm, tn;
             tile_coords(x, ntm, ntn, tm, tn);
             const long long m0 = tm * BM, n0 = tn * BN;
-            if (FT) {
+            if (FT && FTB_WSX_NOSIDE) {  // timing experiment: no loads, thresholds that never flag
+                WsSide &sd = side[buf & (RB - 1)];
+                sd.nrm_row[et] = 1e300; sd.pre_r[et] = 0.0; sd.nrm_col[et] = 1e300; sd.pre_s[et] = 0.0;
+                if (et == 0) {
+                    sd.nrm_max[0] = sd.nrm_max[1] = 1e300;
+                    flags[buf & (RB - 1)][0] = 0;
+                    flags[buf & (RB - 1)][1] = 0;
+                }
+                if (et == 32) plan_rng[buf & (RB - 1)][0] = plan_rng[buf & (RB - 1)][1] = 0;
+            }
+            if (FT && !FTB_WSX_NOSIDE) {
                 const long long mvalid = min((long long)BM, g.M - m0), nvalid = min((long long)BN, g.N - n0);
                 const long long gi = m0 + et, gj = n0 + et;
                 WsSide &sd = side[buf & (RB - 1)];
-                // the encode pass's per-k-chunk partials and the checksum GEMMs' k-split partials,
-                // summed here in index order (no side_finalize_kernel launch on this path)
-                sd.nrm_row[et] = et < mvalid ? sum_strided_ro(g.lineA + gi, g.M, g.kch) : 0.0;
-                sd.pre_r[et] = et < mvalid ? sum_strided_ro(g.Rpre + tn * g.M + gi, g.stride_r, g.splits_r) : 0.0;
-                sd.nrm_col[et] = et < nvalid ? sum_strided_ro(g.lineB + gj, g.N, g.kchB) : 0.0;
-                sd.pre_s[et] = et < nvalid ? sum_strided_ro(g.Spre + tm * g.N + gj, g.stride_s, g.splits_s) : 0.0;
+                // the finalized side data (side_finalize_kernel: the encode pass's per-k-chunk
+                // partials and the checksum GEMMs' k-split partials summed once, in index order):
+                // plain copies, no FP64 instruction in the epilogue warps
+                sd.nrm_row[et] = et < mvalid ? ld_ro(g.fin_nrmA + gi) : 0.0;
+                sd.pre_r[et] = et < mvalid ? ld_ro(g.fin_R + tn * g.M + gi) : 0.0;
+                sd.nrm_col[et] = et < nvalid ? ld_ro(g.fin_nrmB + gj) : 0.0;
+                sd.pre_s[et] = et < nvalid ? ld_ro(g.fin_S + tm * g.N + gj) : 0.0;
                 if (et == 0) {
-                    sd.nrm_max[0] = max_strided_ro(g.tmaxA + tm, ntm, g.kch);
-                    sd.nrm_max[1] = max_strided_ro(g.tmaxB + tn, ntn, g.kchB);
+                    sd.nrm_max[0] = ld_ro(g.fin_maxA + tm);
+                    sd.nrm_max[1] = ld_ro(g.fin_maxB + tn);
                     flags[buf & (RB - 1)][0] = 0;
                     flags[buf & (RB - 1)][1] = 0;
                 }
@@ -632,8 +646,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         //   words alike (integer pipe) -> shared memory; then every MMA thread verifies one row or
         //   column of the tile (readings R3, R4, R4k) and lists it if flagged.
         // The FP64 work runs while no warp of the SM issues DMMAs (mma_bar before and after).
-        auto finish_tile = [&](long long x, int it, auto bm_c) {
+        auto finish_tile = [&](long long x, int it, auto bm_c, auto full_c) {
             constexpr int BMODE = decltype(bm_c)::value;  // 0: beta = 0, 1: beta = 1, 2: other
+            // M and N multiples of the tile: no element of any tile lies outside M x N, and the
+            // validity masks of d (~35 % of the tail's instructions: bit tests and selects per
+            // element) are compiled out
+            constexpr bool ALLFULL = decltype(full_c)::value != 0;
             long long tm, tn;
             tile_coords(x, ntm, ntn, tm, tn);
             const int buf = it & 1, rb = buf & (RB - 1);
@@ -692,12 +710,14 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             const unsigned tb = tbase + ((unsigned)(32 * wm) << 16) + (unsigned)(buf * 256 + wn * 128);
             // validity of this thread's fragment rows a (bit a) and columns (b, e) (bit 2 b + e)
             unsigned vr = 0u, vc = 0u;
+            if (FT && !ALLFULL) {
 #pragma unroll
-            for (int a = 0; a < 4; a++) vr |= (row_of(a) < mvalid ? 1u : 0u) << a;
+                for (int a = 0; a < 4; a++) vr |= (row_of(a) < mvalid ? 1u : 0u) << a;
 #pragma unroll
-            for (int b = 0; b < 8; b++)
+                for (int b = 0; b < 8; b++)
 #pragma unroll
-                for (int e = 0; e < 2; e++) vc |= (col_of(b, e) < nvalid ? 1u : 0u) << (2 * b + e);
+                    for (int e = 0; e < 2; e++) vc |= (col_of(b, e) < nvalid ? 1u : 0u) << (2 * b + e);
+            }
             double rs[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
             for (int bq = 0; bq < 4; bq++) {
@@ -719,7 +739,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                                 const double t = BMODE == 2 ? g.beta * c0 : c0;
                                 const double o = BMODE == 0 ? g.alpha * acc[a][b][e] : fma(g.alpha, acc[a][b][e], t);
                                 if (FT) {
-                                    const bool ok = (vr >> a) & (vc >> (2 * b + e)) & 1u;
+                                    const bool ok = ALLFULL || ((vr >> a) & (vc >> (2 * b + e)) & 1u);
                                     const double d = ok ? (BMODE == 0 ? o : o - t) : 0.0;
                                     rs[a] += d;
                                     cs[2 * bh + e] += d;
@@ -789,10 +809,18 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             mma_bar();  // the partial-sum buffers are free; every warp enters the next tile together
             if (mw == 0 && lane == 0) WS_ADD(WP_MMA_TAIL, ts0);
         };
+        const bool allfull = FT && g.M % BM == 0 && g.N % BN == 0;
         auto finish = [&](long long x, int it) {
-            if (bmode == 0) finish_tile(x, it, IntC<0>{});
-            else if (bmode == 1) finish_tile(x, it, IntC<1>{});
-            else finish_tile(x, it, IntC<2>{});
+            if (FT && allfull) {  // (the masks exist only in the FT tail)
+                constexpr int F = FT ? 1 : 0;
+                if (bmode == 0) finish_tile(x, it, IntC<0>{}, IntC<F>{});
+                else if (bmode == 1) finish_tile(x, it, IntC<1>{}, IntC<F>{});
+                else finish_tile(x, it, IntC<2>{}, IntC<F>{});
+            } else {
+                if (bmode == 0) finish_tile(x, it, IntC<0>{}, IntC<0>{});
+                else if (bmode == 1) finish_tile(x, it, IntC<1>{}, IntC<0>{});
+                else finish_tile(x, it, IntC<2>{}, IntC<0>{});
+            }
         };
         // The ring of operand stages runs across tile boundaries: slot st of round `phase` holds
         // the next k-tile.  The slot is a runtime index, and the tile tail follows the k-tile
