@@ -335,9 +335,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     // they load C0, per row (the row's thread) and per column (per epilogue warp)
     __shared__ unsigned redm_r[RB][FT ? BM : 1], redm_c[RB][FT ? 4 : 1][FT ? BN : 1];
     __shared__ int rflag[FT ? BM : 1], cflag[FT ? BN : 1];
-    // FT, per TMEM buffer: the fault plan's CSR range of its tile (test harness), looked up by the
-    // epilogue warps with the references so that no dependent global load sits in the tile tail
-    __shared__ int plan_rng[RB][2];
+    // FT, per TMEM buffer: the planned flips of its tile (test harness), looked up by the epilogue
+    // warps with the references: their count and, per flip, the MMA thread (32 mw + lane) that owns
+    // the element, its accumulator index k = 16 a + 2 b + e and the bit.  No plan code but one
+    // shared-memory read sits in the MMA warps' tail of a clean tile.
+    __shared__ int hit_n[RB], hit_tid[RB][4], hit_k[RB][4], hit_bit[RB][4];
 #ifdef FTB_WSX_PADSMEM  // timing experiment only: static shared memory of the FT kernel in the non-FT one
     __shared__ double wsx_pad[FT ? 1 : 2816];
     if (threadIdx.x == 0) wsx_pad[blockIdx.x % 2816] = 0.0;
@@ -462,18 +464,45 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                     flags[buf & (RB - 1)][0] = 0;
                     flags[buf & (RB - 1)][1] = 0;
                 }
-                if (et == 32) {  // planned flips of the tile: [lo, hi) of the plan's CSR (empty without a plan)
-                    int lo = 0, hi = 0;
-                    if (g.plan_ptr) {
-                        const long long gtm = tm + g.off_i / BM, gtn = tn + g.off_j / BN;
-                        if (gtm < g.plan_ntm && gtn < g.plan_ntn) {
-                            const long long tix = gtn * g.plan_ntm + gtm;
-                            lo = ld_ro(g.plan_ptr + tix);
-                            hi = ld_ro(g.plan_ptr + tix + 1);
+                // planned flips of the tile: [lo, hi) of the plan's CSR (every thread reads the same
+                // two words); on a tile with flips (rare) each epilogue thread runs the fragment
+                // maps of two MMA threads over the flips and the owner's slot is filled in
+                int lo = 0, hi = 0;
+                if (g.plan_ptr) {
+                    const long long gtm = tm + g.off_i / BM, gtn = tn + g.off_j / BN;
+                    if (gtm < g.plan_ntm && gtn < g.plan_ntn) {
+                        const long long tix = gtn * g.plan_ntm + gtm;
+                        lo = ld_ro(g.plan_ptr + tix);
+                        hi = min(ld_ro(g.plan_ptr + tix + 1), lo + 4);  // FTBLAS_MAX_FLIPS_PER_TILE
+                    }
+                }
+                if (et == 32) hit_n[buf & (RB - 1)] = hi - lo;
+                if (hi > lo) {
+                    if (et < 4) hit_tid[buf & (RB - 1)][et] = -1;
+                    epi_bar();
+                    for (int f = lo; f < hi; f++) {
+                        const long long li = ld_ro(g.plan_i + f) - g.off_i - m0;
+                        const long long lj = ld_ro(g.plan_j + f) - g.off_j - n0;
+#pragma unroll 1
+                        for (int t = et; t < 256; t += 128) {
+                            const int tw = t >> 5, tl = t & 31, twm = tw & 3, twn = tw >> 2;
+                            int k = -1;
+#pragma unroll
+                            for (int a = 0; a < 4; a++)
+#pragma unroll
+                                for (int b = 0; b < 8; b++)
+#pragma unroll
+                                    for (int e = 0; e < 2; e++)
+                                        if (frag_mn<KCA>(twm * 32, a, tl >> 2) == li &&
+                                            frag_mn<KCB>(twn * 64, b, 2 * (tl & 3) + e) == lj)
+                                            k = 16 * a + 2 * b + e;
+                            if (k >= 0) {
+                                hit_tid[buf & (RB - 1)][f - lo] = t;
+                                hit_k[buf & (RB - 1)][f - lo] = k;
+                                hit_bit[buf & (RB - 1)][f - lo] = ld_ro(g.plan_bit + f);
+                            }
                         }
                     }
-                    plan_rng[buf & (RB - 1)][0] = lo;
-                    plan_rng[buf & (RB - 1)][1] = hi;
                 }
             }
             if (!need_c0) return;
@@ -646,65 +675,23 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         //   words alike (integer pipe) -> shared memory; then every MMA thread verifies one row or
         //   column of the tile (readings R3, R4, R4k) and lists it if flagged.
         // The FP64 work runs while no warp of the SM issues DMMAs (mma_bar before and after).
-        auto finish_tile = [&](long long x, int it, auto bm_c, auto full_c) {
+        // Tile tail, part 1 (finish, below): leave the DMMA stream together, wait for the TMEM
+        // buffer, read the tile's planned flips (found by the epilogue warps, prep).  Part 2 is
+        // finish_tile<BMODE, ALLFULL, FLIP>: tiles with planned flips run a copy of the tail that
+        // applies them to the accumulator values as it reads them (compares on static element
+        // indices), clean tiles a copy without any flip code.  (Flipping the accumulator registers
+        // in place through a jump table, one case per register, and searching the hits with the
+        // MMA threads' own fragment maps made ptxas shuffle the accumulators through ~360 moves
+        // per tile tail: 2.2 % at K = 256.)
+        auto finish_tile = [&](long long x, int it, long long tm, long long tn, const int (&hk)[4],
+                               const int (&hb)[4], auto bm_c, auto full_c, auto flip_c) {
             constexpr int BMODE = decltype(bm_c)::value;  // 0: beta = 0, 1: beta = 1, 2: other
             // M and N multiples of the tile: no element of any tile lies outside M x N, and the
             // validity masks of d (~35 % of the tail's instructions: bit tests and selects per
             // element) are compiled out
             constexpr bool ALLFULL = decltype(full_c)::value != 0;
-            long long tm, tn;
-            tile_coords(x, ntm, ntn, tm, tn);
+            constexpr bool FLIP = decltype(flip_c)::value != 0;
             const int buf = it & 1, rb = buf & (RB - 1);
-            WS_T(te0);
-            // all MMA warps leave the DMMA stream together and enter the next tile together: an
-            // FP64 instruction issued beside another warp's DMMA stream waits ~75 cycles for the
-            // pipe (tools/fp64_side.cu)
-            mma_bar();
-            ws_wait(&buf_ready[buf], (unsigned)((it >> 1) & 1));
-            tc_fence_after();
-            // planned flips of this tile (test harness; after the buffer wait: plan_rng is the
-            // epilogue's): each thread collects the hits on its own
-            // 64 elements (index k = 16 a + 2 b + e; at most FTBLAS_MAX_FLIPS_PER_TILE = 4 per
-            // tile, checked by ftblas_set_fault_plan), then flips each through a jump table
-            int hk[4] = {-1, -1, -1, -1}, hb[4] = {0, 0, 0, 0};
-            if (FT) {
-                // [lo, hi) of the plan's CSR, looked up by the epilogue warps with the tile's
-                // references (prep): no dependent global load in the tail of a clean tile
-                const int lo = plan_rng[rb][0], hi = plan_rng[rb][1];
-                {
-                    for (int f = lo; f < hi; f++) {
-                        const long long li = ld_ro(g.plan_i + f) - g.off_i - tm * BM;
-                        const long long lj = ld_ro(g.plan_j + f) - g.off_j - tn * BN;
-                        int k = -1;
-#pragma unroll
-                        for (int a = 0; a < 4; a++)
-#pragma unroll
-                            for (int b = 0; b < 8; b++)
-#pragma unroll
-                                for (int e = 0; e < 2; e++)
-                                    if (row_of(a) == li && col_of(b, e) == lj) k = 16 * a + 2 * b + e;
-                        if (k < 0) continue;
-                        hk[3] = hk[2]; hb[3] = hb[2]; hk[2] = hk[1]; hb[2] = hb[1];
-                        hk[1] = hk[0]; hb[1] = hb[0]; hk[0] = k; hb[0] = ld_ro(g.plan_bit + f);
-                    }
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < 4; q++)
-                if (hk[q] >= 0) {
-                    // one accumulator register per case (a jump table): the accumulators stay in place
-                    const long long m = 1ll << hb[q];
-                    switch (hk[q]) {
-#define FTB_FLIP_CASE(K) case K: acc[(K) >> 4][((K) >> 1) & 7][(K) & 1] = __longlong_as_double(__double_as_longlong(acc[(K) >> 4][((K) >> 1) & 7][(K) & 1]) ^ m); break;
-#define FTB_FLIP_CASE8(K) FTB_FLIP_CASE(K) FTB_FLIP_CASE(K + 1) FTB_FLIP_CASE(K + 2) FTB_FLIP_CASE(K + 3) FTB_FLIP_CASE(K + 4) FTB_FLIP_CASE(K + 5) FTB_FLIP_CASE(K + 6) FTB_FLIP_CASE(K + 7)
-                        FTB_FLIP_CASE8(0) FTB_FLIP_CASE8(8) FTB_FLIP_CASE8(16) FTB_FLIP_CASE8(24)
-                        FTB_FLIP_CASE8(32) FTB_FLIP_CASE8(40) FTB_FLIP_CASE8(48) FTB_FLIP_CASE8(56)
-#undef FTB_FLIP_CASE8
-#undef FTB_FLIP_CASE
-                        default: break;
-                    }
-                }
-            if (mw == 0 && lane == 0) WS_ADD(WP_MMA_WAIT_BUF, te0);
             WS_T(ts0);
             const long long mvalid = min((long long)BM, g.M - tm * BM), nvalid = min((long long)BN, g.N - tn * BN);
             const unsigned tb = tbase + ((unsigned)(32 * wm) << 16) + (unsigned)(buf * 256 + wn * 128);
@@ -737,7 +724,14 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                                 const int a = 2 * p + h, b = 2 * bq + bh;
                                 const double c0 = v[bh][h][e];
                                 const double t = BMODE == 2 ? g.beta * c0 : c0;
-                                const double o = BMODE == 0 ? g.alpha * acc[a][b][e] : fma(g.alpha, acc[a][b][e], t);
+                                double av = acc[a][b][e];
+                                if (FLIP) {
+#pragma unroll
+                                    for (int q = 0; q < 4; q++)
+                                        if (hk[q] == 16 * a + 2 * b + e)
+                                            av = __longlong_as_double(__double_as_longlong(av) ^ (1ll << hb[q]));
+                                }
+                                const double o = BMODE == 0 ? g.alpha * av : fma(g.alpha, av, t);
                                 if (FT) {
                                     const bool ok = ALLFULL || ((vr >> a) & (vc >> (2 * b + e)) & 1u);
                                     const double d = ok ? (BMODE == 0 ? o : o - t) : 0.0;
@@ -811,16 +805,38 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         };
         const bool allfull = FT && g.M % BM == 0 && g.N % BN == 0;
         auto finish = [&](long long x, int it) {
-            if (FT && allfull) {  // (the masks exist only in the FT tail)
-                constexpr int F = FT ? 1 : 0;
-                if (bmode == 0) finish_tile(x, it, IntC<0>{}, IntC<F>{});
-                else if (bmode == 1) finish_tile(x, it, IntC<1>{}, IntC<F>{});
-                else finish_tile(x, it, IntC<2>{}, IntC<F>{});
-            } else {
-                if (bmode == 0) finish_tile(x, it, IntC<0>{}, IntC<0>{});
-                else if (bmode == 1) finish_tile(x, it, IntC<1>{}, IntC<0>{});
-                else finish_tile(x, it, IntC<2>{}, IntC<0>{});
+            long long tm, tn;
+            tile_coords(x, ntm, ntn, tm, tn);
+            const int buf = it & 1, rb = buf & (RB - 1);
+            WS_T(te0);
+            // all MMA warps leave the DMMA stream together and enter the next tile together: an
+            // FP64 instruction issued beside another warp's DMMA stream waits ~75 cycles for the
+            // pipe (tools/fp64_side.cu)
+            mma_bar();
+            ws_wait(&buf_ready[buf], (unsigned)((it >> 1) & 1));
+            tc_fence_after();
+            // planned flips of this tile (test harness): found by the epilogue warps (prep)
+            int hk[4] = {-1, -1, -1, -1}, hb[4] = {0, 0, 0, 0};
+            const int nh = FT ? hit_n[rb] : 0;
+            const bool anyflip = nh > 0;  // CTA-uniform
+            if (FT && anyflip) {
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    if (q < nh && hit_tid[rb][q] == 32 * mw + lane) {
+                        hk[q] = hit_k[rb][q];
+                        hb[q] = hit_bit[rb][q];
+                    }
             }
+            if (mw == 0 && lane == 0) WS_ADD(WP_MMA_WAIT_BUF, te0);
+            auto go = [&](auto full_c, auto flip_c) {
+                if (bmode == 0) finish_tile(x, it, tm, tn, hk, hb, IntC<0>{}, full_c, flip_c);
+                else if (bmode == 1) finish_tile(x, it, tm, tn, hk, hb, IntC<1>{}, full_c, flip_c);
+                else finish_tile(x, it, tm, tn, hk, hb, IntC<2>{}, full_c, flip_c);
+            };
+            constexpr int F = FT ? 1 : 0;  // (masks and flips exist only in the FT tail)
+            if (FT && anyflip) go(IntC<0>{}, IntC<F>{});
+            else if (FT && allfull) go(IntC<F>{}, IntC<0>{});
+            else go(IntC<0>{}, IntC<0>{});
         };
         // The ring of operand stages runs across tile boundaries: slot st of round `phase` holds
         // the next k-tile.  The slot is a runtime index, and the tile tail follows the k-tile

@@ -13,14 +13,18 @@ names = ["mma_wait_full", "mma_wait_buf", "mma_tail", "epi_wait_acc", "epi_c0loa
 w = syn.CONFIG_BY_NAME[sys.argv[1]]
 mode = sys.argv[2] if len(sys.argv) > 2 else "ft"
 d = syn.make_inputs(w)
+nfl = int(os.environ.get("FLIPS", "0"))  # FLIPS=n: a seeded fault plan of n flips (development: which phase the flagged tiles stretch)
 ft.ftblas_set_stream(None); ft.ftblas_set_tile_policy("ws")
 A_t, pA = to_dev(d["A"]); B_t, pB = to_dev(d["B"]); C_t, pC = to_dev(d["C"])
 L = ft.lib
+if nfl:
+    ft.ftblas_set_fault_plan(*syn.fault_plan(w.M, w.N, nfl, w.seed))
+rep = ft.Report(4 * nfl + 16)
 L.ftblas_ws_prof_read.argtypes = [ct.POINTER(ct.c_ulonglong), ct.c_int]
 buf = (ct.c_ulonglong * (1024 * 16))()
 def call():
     if mode == "ft":
-        ft.ftblas_dgemm(w.transA, w.transB, w.M, w.N, w.K, w.alpha, pA, d["lda"], pB, d["ldb"], w.beta, pC, d["ldc"], None)
+        ft.ftblas_dgemm(w.transA, w.transB, w.M, w.N, w.K, w.alpha, pA, d["lda"], pB, d["ldb"], w.beta, pC, d["ldc"], rep if nfl else None)
     else:
         ft.ftblas_dgemm_noft(w.transA, w.transB, w.M, w.N, w.K, w.alpha, pA, d["lda"], pB, d["ldb"], w.beta, pC, d["ldc"])
 for _ in range(3): call()
@@ -32,3 +36,5 @@ a = np.array(buf[:148 * 16], dtype=np.float64).reshape(148, 16) / 1e3  # us
 print(f"{w.name} {mode}: call {e0.elapsed_time(e1):.3f} ms; per-CTA phase sums (us): mean / max")
 for k, n in enumerate(names):
     print(f"  {n:18s} {a[:, k].mean():10.1f} {a[:, k].max():10.1f}")
+if nfl:
+    print("  located", rep.count, "of", nfl, "; CTAs by mma_total:", np.argsort(-a[:, 11])[:6], np.sort(-a[:, 11])[:6] * -1)
