@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                     flags[buf & (RB - 1)][0] = 0;
                     flags[buf & (RB - 1)][1] = 0;
                 }
-                if (et == 32) plan_rng[buf & (RB - 1)][0] = plan_rng[buf & (RB - 1)][1] = 0;
+                if (et == 32) hit_n[buf & (RB - 1)] = 0;
             }
             if (FT && !FTB_WSX_NOSIDE) {
                 const long long mvalid = min((long long)BM, g.M - m0), nvalid = min((long long)BN, g.N - n0);
@@ -676,21 +676,20 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         //   column of the tile (readings R3, R4, R4k) and lists it if flagged.
         // The FP64 work runs while no warp of the SM issues DMMAs (mma_bar before and after).
         // Tile tail, part 1 (finish, below): leave the DMMA stream together, wait for the TMEM
-        // buffer, read the tile's planned flips (found by the epilogue warps, prep).  Part 2 is
-        // finish_tile<BMODE, ALLFULL, FLIP>: tiles with planned flips run a copy of the tail that
-        // applies them to the accumulator values as it reads them (compares on static element
-        // indices), clean tiles a copy without any flip code.  (Flipping the accumulator registers
-        // in place through a jump table, one case per register, and searching the hits with the
-        // MMA threads' own fragment maps made ptxas shuffle the accumulators through ~360 moves
-        // per tile tail: 2.2 % at K = 256.)
-        auto finish_tile = [&](long long x, int it, long long tm, long long tn, const int (&hk)[4],
-                               const int (&hb)[4], auto bm_c, auto full_c, auto flip_c) {
+        // buffer, apply the tile's planned flips (found by the epilogue warps, prep; rare): a thread
+        // with a hit copies its accumulators to a local array, flips there (dynamic index) and
+        // copies back, so the accumulator registers themselves are only ever indexed statically.
+        // (Flipping them in place through a jump table, one case per register, and searching the
+        // hits with the MMA threads' own fragment maps made ptxas shuffle the accumulators through
+        // ~360 moves per tile tail: 2.2 % at K = 256; a separate copy of the tail for flagged
+        // tiles ran ~27 us per flagged tile, its code fetched cold.)  Part 2 is
+        // finish_tile<BMODE, ALLFULL>.
+        auto finish_tile = [&](long long x, int it, long long tm, long long tn, auto bm_c, auto full_c) {
             constexpr int BMODE = decltype(bm_c)::value;  // 0: beta = 0, 1: beta = 1, 2: other
             // M and N multiples of the tile: no element of any tile lies outside M x N, and the
             // validity masks of d (~35 % of the tail's instructions: bit tests and selects per
             // element) are compiled out
             constexpr bool ALLFULL = decltype(full_c)::value != 0;
-            constexpr bool FLIP = decltype(flip_c)::value != 0;
             const int buf = it & 1, rb = buf & (RB - 1);
             WS_T(ts0);
             const long long mvalid = min((long long)BM, g.M - tm * BM), nvalid = min((long long)BN, g.N - tn * BN);
@@ -724,14 +723,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                                 const int a = 2 * p + h, b = 2 * bq + bh;
                                 const double c0 = v[bh][h][e];
                                 const double t = BMODE == 2 ? g.beta * c0 : c0;
-                                double av = acc[a][b][e];
-                                if (FLIP) {
-#pragma unroll
-                                    for (int q = 0; q < 4; q++)
-                                        if (hk[q] == 16 * a + 2 * b + e)
-                                            av = __longlong_as_double(__double_as_longlong(av) ^ (1ll << hb[q]));
-                                }
-                                const double o = BMODE == 0 ? g.alpha * av : fma(g.alpha, av, t);
+                                const double o = BMODE == 0 ? g.alpha * acc[a][b][e] : fma(g.alpha, acc[a][b][e], t);
                                 if (FT) {
                                     const bool ok = ALLFULL || ((vr >> a) & (vc >> (2 * b + e)) & 1u);
                                     const double d = ok ? (BMODE == 0 ? o : o - t) : 0.0;
@@ -816,27 +808,36 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             ws_wait(&buf_ready[buf], (unsigned)((it >> 1) & 1));
             tc_fence_after();
             // planned flips of this tile (test harness): found by the epilogue warps (prep)
-            int hk[4] = {-1, -1, -1, -1}, hb[4] = {0, 0, 0, 0};
             const int nh = FT ? hit_n[rb] : 0;
-            const bool anyflip = nh > 0;  // CTA-uniform
-            if (FT && anyflip) {
+            if (FT && nh > 0) {  // CTA-uniform, rare
+                int hk[4] = {-1, -1, -1, -1}, hb[4] = {0, 0, 0, 0};
 #pragma unroll
                 for (int q = 0; q < 4; q++)
                     if (q < nh && hit_tid[rb][q] == 32 * mw + lane) {
                         hk[q] = hit_k[rb][q];
                         hb[q] = hit_bit[rb][q];
                     }
+                if ((hk[0] & hk[1] & hk[2] & hk[3]) >= 0) {  // this thread owns a planned element
+                    long long tmp[64];
+#pragma unroll
+                    for (int k = 0; k < 64; k++) tmp[k] = __double_as_longlong(acc[k >> 4][(k >> 1) & 7][k & 1]);
+#pragma unroll
+                    for (int q = 0; q < 4; q++)
+                        if (hk[q] >= 0) tmp[hk[q]] ^= 1ll << hb[q];
+#pragma unroll
+                    for (int k = 0; k < 64; k++) acc[k >> 4][(k >> 1) & 7][k & 1] = __longlong_as_double(tmp[k]);
+                }
+                __syncwarp();  // reconverged before the .sync.aligned tcgen05 operations of the tail
             }
             if (mw == 0 && lane == 0) WS_ADD(WP_MMA_WAIT_BUF, te0);
-            auto go = [&](auto full_c, auto flip_c) {
-                if (bmode == 0) finish_tile(x, it, tm, tn, hk, hb, IntC<0>{}, full_c, flip_c);
-                else if (bmode == 1) finish_tile(x, it, tm, tn, hk, hb, IntC<1>{}, full_c, flip_c);
-                else finish_tile(x, it, tm, tn, hk, hb, IntC<2>{}, full_c, flip_c);
+            auto go = [&](auto full_c) {
+                if (bmode == 0) finish_tile(x, it, tm, tn, IntC<0>{}, full_c);
+                else if (bmode == 1) finish_tile(x, it, tm, tn, IntC<1>{}, full_c);
+                else finish_tile(x, it, tm, tn, IntC<2>{}, full_c);
             };
-            constexpr int F = FT ? 1 : 0;  // (masks and flips exist only in the FT tail)
-            if (FT && anyflip) go(IntC<0>{}, IntC<F>{});
-            else if (FT && allfull) go(IntC<F>{}, IntC<0>{});
-            else go(IntC<0>{}, IntC<0>{});
+            constexpr int F = FT ? 1 : 0;  // (the masks exist only in the FT tail)
+            if (FT && allfull) go(IntC<F>{});
+            else go(IntC<0>{});
         };
         // The ring of operand stages runs across tile boundaries: slot st of round `phase` holds
         // the next k-tile.  The slot is a runtime index, and the tile tail follows the k-tile
