@@ -163,7 +163,7 @@ int ftblas_report_fetch(ftblas_err_report *err_report);
  * epilogue.  Host arrays, copied.  n == 0 clears the plan.  Plans are matched
  * against the M x N of each call; entries outside it are ignored.  At most
  * FTBLAS_MAX_FLIPS_PER_TILE flips may fall into one FTBLAS_TILE_M x FTBLAS_TILE_N
- * tile (the persistent kernel keeps each thread's hits in registers); a plan
+ * tile (the persistent kernel keeps a tile's hits in a 4-entry shared-memory list); a plan
  * with more returns -1 and leaves the installed plan unchanged.  Returns -1 for
  * n < 0, -2 for NULL arrays or negative coordinates, -4 for a bit outside 0..63. */
 #define FTBLAS_MAX_FLIPS_PER_TILE 4

@@ -17,14 +17,16 @@
 //             verifies one row or column of the tile against the checksum-GEMM references
 //             (readings R4, R4k) and lists it if flagged; then the warps start
 //             the next tile.  The FP64 epilogue arithmetic thus runs in the warps that own the
-//             FP64 pipe, about 1.8 us per tile (FT) while no warp issues DMMAs, instead of beside
+//             FP64 pipe, about 1.6 us per tile (FT) while no warp issues DMMAs, instead of beside
 //             the DMMA stream (where an FP64 instruction of another warp waits ~75 cycles for an
 //             issue slot, tools/fp64_side.cu);
 //   epilogue  (4 warps, one TMEM lane = one tile row per thread): locate (lines 540, 521;
 //             readings R5-R7: candidates of flagged rows x columns listed for correct_kernel),
 //             store the verified tile from TMEM to C, and load the C0 (with its |C0| row / column
-//             maxima, integer pipe) and the verification references of the tile after next into
-//             the freed TMEM buffer / shared memory.
+//             maxima, integer pipe), the verification references (plain copies of
+//             side_finalize_kernel's sums: no FP64 instruction is issued here) and the planned
+//             flips (test harness: a hit list) of the tile after next into the freed TMEM buffer /
+//             shared memory.
 // TMEM: 2 buffers x 256 columns x 128 lanes x 32 bit = all 512 columns, lane = tile row.  MMA
 // warp w reads / writes with the 16x256b shape (a thread of fragment row g owns lanes g and
 // g + 8: the mma.sync accumulator layout), so fragments a = 2p, 2p + 1 sit in lanes
